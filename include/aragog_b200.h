@@ -1,0 +1,181 @@
+/*
+ * aragog_b200.h -- C ABI of the B200-native (sm_100a) implementation of
+ * Aragog's two data-parallel hot paths (arXiv 2511.20975):
+ *
+ *   1. one-time routing: enumerate the mixed-radix configuration space of a
+ *      batch of requests, score every configuration with the binary accuracy
+ *      router, stream-compact the accuracy-preserving set (enumerate mode),
+ *      or replay the chain/binary-search predictor (chain mode);
+ *   2. per-stage just-in-time scheduling: beam-search round decisions,
+ *      prefix pruning, and the runtime-cost re-cost + argmin.
+ *
+ * Plain C types only (no torch, no C++).  Device-pointer entry points are
+ * asynchronous on the context's stream; *_host entry points take host buffers
+ * and include the host<->device copies.
+ *
+ * Every entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).  Status codes mirror the
+ * reference's exception taxonomy (include/aragog/errors.h:22-34,
+ * tools/main.cpp:290-303): ValidationError -> AG_ERR_VALIDATION,
+ * IoError -> AG_ERR_IO, std::logic_error -> AG_ERR_INTERNAL.
+ */
+#ifndef ARAGOG_B200_H
+#define ARAGOG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AG_OK 0
+#define AG_ERR_INTERNAL 1
+#define AG_ERR_VALIDATION 2
+#define AG_ERR_IO 3
+#define AG_ERR_CUDA 4
+
+#define AG_ROUTER_ORACLE 0 /* OracleRouter, include/aragog/router.h:43-53 */
+#define AG_ROUTER_NOISY 1  /* NoisyRouter over an oracle, router.h:57-70 */
+
+#define AG_FORCE_TOP 1u /* top is always a member (predictor.cpp:177,255) */
+
+/* Message of the last failing call on this thread. */
+const char* ag_last_error(void);
+int ag_abi_version(void);
+
+/* ======================================================================== *
+ * Configuration space                                                       *
+ * ======================================================================== */
+typedef struct ag_space ag_space;
+
+/* WorkflowGraph::build + ModelCatalog + ConfigSpace
+ * (include/aragog/workflow.h:34-152; src/workflow.cpp:38-173,209-224).
+ * edges: n_edges (from, to) pairs of declaration indices.  cost strictly
+ * increasing, slot_throughput strictly decreasing (workflow.cpp:38-60).
+ * The GPU path additionally requires M^N <= 2^32 and N <= 32. */
+int ag_space_create(int n_agents, int n_edges, const int32_t* edges,
+                    int n_models, const double* cost,
+                    const double* slot_throughput, ag_space** out);
+void ag_space_destroy(ag_space* space);
+/* decl[pos] = declaration index at canonical position, depth[pos]
+ * (WorkflowGraph::declaration_index/depth, workflow.h:68-77); size = M^N. */
+int ag_space_info(const ag_space* space, int32_t* n_agents, int32_t* n_models,
+                  int32_t* decl, int32_t* depth, uint64_t* size);
+
+/* ======================================================================== *
+ * Device context                                                            *
+ * ======================================================================== */
+typedef struct ag_ctx ag_ctx;
+
+int ag_ctx_create(const ag_space* space, int device, ag_ctx** out);
+void ag_ctx_destroy(ag_ctx* ctx);
+/* cudaStream_t as void*; NULL = the legacy default stream */
+int ag_ctx_set_stream(ag_ctx* ctx, void* stream);
+int ag_ctx_synchronize(ag_ctx* ctx);
+/* number of kernels this context launched since creation */
+uint64_t ag_ctx_launch_count(const ag_ctx* ctx);
+
+/* Live per-kernel profile: while enabled every launch is bracketed by CUDA
+ * events on the context stream.  ag_ctx_profile_end synchronises the stream
+ * and returns, per kernel id (0 .. AG_NUM_KERNELS-1), the summed device
+ * milliseconds and launch counts since ag_ctx_profile_begin. */
+#define AG_NUM_KERNELS 9
+int ag_ctx_profile_begin(ag_ctx* ctx);
+int ag_ctx_profile_end(ag_ctx* ctx, double* ms, uint64_t* launches);
+const char* ag_kernel_name(int kernel_id);
+
+/* pinned host / device memory helpers */
+int ag_host_alloc(size_t bytes, void** out);
+int ag_host_free(void* p);
+int ag_device_alloc(size_t bytes, void** out);
+int ag_device_free(void* p);
+
+/* ======================================================================== *
+ * Routing (hot path 1)                                                      *
+ * ======================================================================== */
+
+/* RouterBackend (router.h:33-41) as data.  kind ORACLE: verdict =
+ * AccurateSet::contains (accuracy.cpp:116-124).  kind NOISY: NoisyRouter over
+ * the oracle (router.cpp:50-57) with fp, fn in [0,1] and noise_seed. */
+typedef struct {
+  int32_t kind;
+  double fp, fn;
+  uint64_t noise_seed;
+  double eval_latency; /* seconds charged per evaluation (predict only) */
+} ag_router;
+
+/* A batch of AccurateSets (accuracy.h:34-40), one row per request, CSR.
+ * seeds: rows of N digits in canonical agent order; removed: canonical
+ * indices.  request_ids: the RequestId each row answers to (router noise is
+ * keyed on it, router.cpp:53-54).  All pointers device-resident for the
+ * device entry points, host-resident for *_host. */
+typedef struct {
+  int32_t n_requests;
+  const uint64_t* request_ids; /* [R] */
+  const int32_t* seed_ptr;     /* [R+1] */
+  const uint8_t* seeds;        /* [seed_ptr[R] * N] */
+  const int32_t* removed_ptr;  /* [R+1] */
+  const uint64_t* removed;     /* [removed_ptr[R]] */
+} ag_truth;
+
+/* Outputs of enumerate mode (device pointers).
+ *   bitmap  [R * W] (W = ceil((end-begin)/32)): bit j of word w of request r
+ *           <-> canonical index begin + 32w + j.  May be NULL.
+ *   counts  [R]   members per request (required).
+ *   offsets [R+1] exclusive scan of counts; may be NULL unless indices set.
+ *   indices [capacity] the members of every request in canonical order,
+ *           request r at [offsets[r], offsets[r+1]).  NULL = bitmap only.
+ *   overflow (device uint32) set to 1 when offsets[R] > capacity; members
+ *           past capacity are not written. May be NULL. */
+typedef struct {
+  uint32_t* bitmap;
+  uint64_t* counts;
+  uint64_t* offsets;
+  uint32_t* indices;
+  uint64_t capacity;
+  uint32_t* overflow;
+} ag_route_out;
+
+/* Enumerate mode over the index range [begin, end) of every request:
+ * verdict = router.evaluate(request_ids[r], at_index(i)) for each i, members
+ * compacted in canonical order.  Replaces enumerate_members
+ * (include/aragog/accuracy.h:81-82, src/accuracy.cpp:227-238) and the
+ * exhaustive oracle set (tests/acceptance/criteria.cpp:93-101) without the
+ * 4096-config guard; [begin, end) sub-ranges shard a deep space across GPUs
+ * (ranks concatenate in rank order = canonical order). */
+int ag_route_enumerate(ag_ctx* ctx, const ag_truth* truth_dev,
+                       const ag_router* router, uint64_t begin, uint64_t end,
+                       uint32_t flags, const ag_route_out* out_dev);
+
+/* Same call with host buffers, copies included (the e2e path).  counts [R],
+ * offsets [R+1], indices [capacity] are host arrays (pinned recommended);
+ * total receives offsets[R].  Returns AG_ERR_VALIDATION if capacity is too
+ * small (total is still reported). */
+int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* truth_host,
+                            const ag_router* router, uint64_t begin,
+                            uint64_t end, uint32_t flags, uint64_t* counts,
+                            uint64_t* offsets, uint32_t* indices,
+                            uint64_t capacity, uint64_t* total);
+
+/* ======================================================================== *
+ * Host-side input synthesis (reference generators; not on the hot path)     *
+ * ======================================================================== */
+typedef struct {
+  double p_easy, p_medium, p_hard, easy_base_prob, violation_rate;
+} ag_gen_params;
+
+/* generate_accurate_set for request ids first_id .. first_id+count-1
+ * (src/accuracy.cpp:144-198; AccuracyGenParams accuracy.h:42-52).
+ * Writes seed_ptr[count+1], seeds (cap seeds_cap rows), removed_ptr[count+1],
+ * removed (cap removed_cap). */
+int ag_generate_truth(const ag_space* space, const ag_gen_params* params,
+                      uint64_t seed, uint64_t salt, uint64_t first_id,
+                      int32_t count, int32_t* seed_ptr, uint8_t* seeds,
+                      int32_t seeds_cap, int32_t* removed_ptr,
+                      uint64_t* removed, int32_t removed_cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,6 @@
+"""B200-native (sm_100a) implementation of Aragog's two data-parallel hot
+paths (arXiv 2511.20975): routing (enumerate / chain modes) and per-stage
+just-in-time scheduling, behind the C ABI in include/aragog_b200.h."""
+from ._capi import AgError, ValidationError, lib  # noqa: F401
+from .routing import (AccuracyBatch, ConfigSpace, Device, DeviceAccuracyBatch,  # noqa: F401
+                      GenParams, NoisyRouter, OracleRouter, RouteResult, enumerate_members)

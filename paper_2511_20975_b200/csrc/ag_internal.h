@@ -1,0 +1,106 @@
+// Internal (C++) definitions behind the opaque C handles.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "ag_common.cuh"
+
+struct ag_space {
+  int n = 0, m = 0;
+  std::vector<int32_t> decl;     // canonical pos -> declaration index
+  std::vector<int32_t> depth;    // by canonical pos
+  std::vector<uint64_t> pred;    // predecessor bitmask by canonical pos
+  std::vector<uint64_t> succ;    // successor bitmask by canonical pos
+  std::vector<double> cost;      // ModelSpec::cost by tier
+  std::vector<double> weight;    // ModelSpec::slot_throughput by tier
+  uint64_t size = 0;             // M^N (0 when > 2^64)
+  bool gpu_ok = false;           // M^N <= 2^32 and N <= 32
+
+  agb::SpaceDev dev() const {
+    agb::SpaceDev s;
+    s.n = n;
+    s.m = m;
+    s.size = size;
+    // ceil(2^64 / m) for m >= 2
+    s.div_m = (~0ULL) / (uint64_t)m + 1;
+    return s;
+  }
+};
+
+namespace agb {
+
+// grow-only device scratch buffer
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  ~Scratch();
+};
+
+}  // namespace agb
+
+namespace agb {
+
+// kernel ids for the live per-kernel CUDA-event profile (bench.py roofline)
+enum KernelId {
+  K_ROUTE_SCORE = 0,
+  K_CHUNK_SCAN,
+  K_REQUEST_SCAN,
+  K_ROUTE_COMPACT,
+  K_PREDICT,
+  K_SCHED_ROUND,
+  K_SCHED_APPLY,
+  K_SCHED_PREP,
+  K_COST_ARGMIN,
+  K_NUM_KERNELS
+};
+extern const char* const kKernelNames[K_NUM_KERNELS];
+
+struct ProfRecord {
+  int kernel;
+  cudaEvent_t start, stop;
+};
+
+}  // namespace agb
+
+struct ag_ctx {
+  const ag_space* space = nullptr;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint64_t launches = 0;
+  // live profile: CUDA events around every launch while enabled
+  bool profiling = false;
+  std::vector<agb::ProfRecord> prof;
+  std::vector<cudaEvent_t> event_pool;
+  // routing scratch
+  agb::Scratch chunk_counts, chunk_off, bitmap, counts, offsets, overflow;
+  agb::Scratch colmask;  // per-space last-digit masks (route 2-D path)
+  int colmask_m = 0;
+  // host-path staging
+  agb::Scratch h_truth;
+  agb::Scratch d_out_idx;
+};
+
+namespace agb {
+
+// Brackets one kernel launch with CUDA events on the context stream when the
+// live profile is enabled, and counts the launch.
+struct Launch {
+  ag_ctx* c;
+  int k;
+  cudaEvent_t e0 = nullptr;
+  Launch(ag_ctx* ctx, int kernel);
+  ~Launch();
+};
+
+int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r,
+                    uint64_t begin, uint64_t end, uint32_t flags,
+                    const ag_route_out* out);
+int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32_t* bitmap,
+                  const uint64_t* offsets, uint32_t* indices, uint64_t capacity);
+int make_router(const ag_router* r, RouterDev* out);
+
+}  // namespace agb

@@ -1,0 +1,690 @@
+// Routing hot path, enumerate mode (K1 score -> K2 scans -> K3 compact).
+//
+// Replaces the exhaustive scoring loop of enumerate_members
+// (reference src/accuracy.cpp:227-238) / oracle_accurate_set
+// (tests/acceptance/criteria.cpp:93-101) driven through
+// RouterBackend::evaluate (include/aragog/router.h:33-41).
+//
+// Work decomposition: a warp-task is up to 1024 consecutive 32-index bitmap
+// words (32K canonical indices) of one request; each of its 32 iterations
+// gives one word to each lane.  Nothing is read per configuration: the
+// configuration is the index.  HBM traffic is the output only (1/8 B per
+// config of bitmap, 4 B per member).
+//
+// Verdict per configuration c (digits d[0..N-1], position 0 most significant):
+//   truth(c)  = c not in removed  &&  exists seed s <= c pointwise
+//             (AccurateSet::contains, accuracy.cpp:116-124)
+//   Write c = (Q, x, l): Q = digits 0..N-3, x = digit N-2, l = digit N-1.
+//   Inside one word l(j) = (l0 + j) mod M for every position j, and (Q, x)
+//   change only at row / block boundaries.  A seed s with s.Q <= Q
+//   contributes the positions with x(j) >= s.x (a suffix of the segment) and
+//   l(j) >= s.l (a periodic mask, tabulated once per space): a word costs
+//   O(#seeds) mask operations instead of O(32 * N) compares.  s.Q <= Q runs
+//   SWAR on packed bytes: ((Q | H) - s.Q) & H == H (all digits < 128).
+//   noisy(c)  = truth ? k >= t_fn : k < t_fp, k = mix({seed, 0xA3, id,
+//             hash_config(c)}) >> 11 (router.cpp:22-28,50-57); the hash chain
+//             is carried incrementally so a scored configuration costs two
+//             splitmix64 finalisers, and only configurations whose verdict
+//             the noise can change are hashed.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <vector>
+
+#include "ag_internal.h"
+
+namespace agb {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kThreads = kWarpsPerBlock * 32;
+constexpr int kMaxFastSeeds = 32;    // per-warp packed-seed cache
+constexpr uint32_t kTaskIters = 32;  // iterations of 32 words per warp-task
+constexpr uint32_t kTaskWords = 32 * kTaskIters;
+
+template <int NT>
+struct DigitsT {
+  static constexpr int kN = NT > 0 ? NT : kMaxAgents;
+};
+
+// thr(row) with per-digit compares (any N <= 32, any M): generic fallback.
+template <int NT>
+__device__ __forceinline__ uint32_t row_threshold(const uint32_t (&d)[DigitsT<NT>::kN], int n,
+                                                  const uint8_t* __restrict__ seeds, int k,
+                                                  uint32_t m) {
+  constexpr int kN = DigitsT<NT>::kN;
+  const int nn = NT > 0 ? NT : n;
+  uint32_t thr = m;
+  for (int s = 0; s < k; ++s) {
+    const uint8_t* sd = seeds + (size_t)s * nn;
+    bool ok = true;
+#pragma unroll
+    for (int a = 0; a < kN - 1; ++a) {
+      if (NT == 0 && a >= nn - 1) break;
+      ok &= (uint32_t)__ldg(sd + a) <= d[a];
+    }
+    const uint32_t last = __ldg(sd + nn - 1);
+    if (ok && last < thr) thr = last;
+  }
+  return thr;
+}
+
+// digits of x (workflow.cpp:263-275)
+template <int NT>
+__device__ __forceinline__ void decode(const SpaceDev& sp, uint32_t x,
+                                       uint32_t (&d)[DigitsT<NT>::kN]) {
+  constexpr int kN = DigitsT<NT>::kN;
+  const int n = NT > 0 ? NT : sp.n;
+  const uint32_t m = (uint32_t)sp.m;
+#pragma unroll
+  for (int a = kN - 1; a >= 0; --a) {
+    if (NT == 0 && a >= n) continue;
+    const uint32_t q = divm(x, sp.div_m);
+    d[a] = x - q * m;
+    x = q;
+  }
+}
+
+// bits [lo, hi) of a 32-bit word, lo/hi clipped to [0, 32]
+__device__ __forceinline__ uint32_t range_bits(int lo, int hi) {
+  lo = max(lo, 0);
+  hi = min(hi, 32);
+  if (lo >= hi) return 0u;
+  return (uint32_t)(((1ull << hi) - 1ull) & ~((1ull << lo) - 1ull));
+}
+
+// Truth word, generic path (row by row).
+template <int NT>
+__device__ __forceinline__ uint32_t truth_word_generic(const SpaceDev& sp, uint32_t i0,
+                                                       uint32_t nbits,
+                                                       const uint8_t* __restrict__ seeds, int k) {
+  constexpr int kN = DigitsT<NT>::kN;
+  const int n = NT > 0 ? NT : sp.n;
+  const uint32_t m = (uint32_t)sp.m;
+  uint32_t d[kN];
+  decode<NT>(sp, i0, d);
+  int pos = -(int)d[n - 1];
+  uint32_t bits = 0;
+  while (pos < (int)nbits) {
+    const uint32_t thr = row_threshold<NT>(d, n, seeds, k, m);
+    bits |= range_bits(pos + (int)thr, pos + (int)m);
+    pos += (int)m;
+    bool carry = true;  // next row: increment digits 0..N-2
+#pragma unroll
+    for (int a = kN - 2; a >= 0; --a) {
+      if (NT == 0 && a >= n - 1) continue;
+      if (carry) {
+        if (++d[a] == m) d[a] = 0;
+        else carry = false;
+      }
+    }
+  }
+  return bits & range_bits(0, (int)nbits);
+}
+
+// Per-warp packed seeds for the 2-D mask path.
+struct PackedSeeds {
+  uint64_t q[kMaxFastSeeds];  // digits 0..N-3, byte b = digit N-3-b
+  uint32_t xl[kMaxFastSeeds]; // digit N-2 in bits 8..15, digit N-1 in bits 0..7
+};
+
+// Digit state of a word start i0 = ((Q * M) + x) * M + l0 for the 2-D path:
+// Q packed as bytes (byte b = digit N-3-b).  Carried from word to word so
+// the hot loop never divides.
+struct WordPos {
+  uint32_t l0, x;
+  uint64_t Q;
+};
+
+__device__ __forceinline__ WordPos word_pos(const SpaceDev& sp, uint32_t i0) {
+  const uint32_t m = (uint32_t)sp.m;
+  WordPos p;
+  const uint32_t y = divm(i0, sp.div_m);
+  p.l0 = i0 - y * m;
+  uint32_t v = divm(y, sp.div_m);
+  p.x = y - v * m;
+  p.Q = 0;
+  for (int b = 0; b < sp.n - 2; ++b) {
+    const uint32_t v2 = divm(v, sp.div_m);
+    p.Q |= (uint64_t)(v - v2 * m) << (8 * b);
+    v = v2;
+  }
+  return p;
+}
+
+// add `inc` (< 128) to the packed block number, propagating carries
+__device__ __forceinline__ uint64_t q_add(uint64_t Q, uint32_t inc, uint32_t m, int nq) {
+  Q += inc;
+  for (int b = 0; b < nq; ++b) {
+    const uint32_t v = (uint32_t)(Q >> (8 * b)) & 0xFFu;
+    if (v < m) break;
+    const uint32_t carry = v / m;
+    Q -= (uint64_t)(carry * m) << (8 * b);
+    if (b + 1 < 8) Q += (uint64_t)carry << (8 * (b + 1));
+  }
+  return Q;
+}
+
+// advance a word position by 32 indices (M <= 32); divisions by M use the
+// precomputed 64-bit reciprocal
+__device__ __forceinline__ void advance32(WordPos& p, uint32_t m, uint64_t div_m, int nq) {
+  const uint32_t l = p.l0 + 32;
+  const uint32_t rows = divm(l, div_m);
+  p.l0 = l - rows * m;
+  const uint32_t xs = p.x + rows;
+  if (xs >= m) {
+    const uint32_t blocks = divm(xs, div_m);
+    p.x = xs - blocks * m;
+    p.Q = q_add(p.Q, blocks, m, nq);
+  } else {
+    p.x = xs;
+  }
+}
+
+// Truth word, 2-D mask path (2 <= N <= 10, M <= 32).
+__device__ __forceinline__ uint32_t truth_word_2d(WordPos p, uint32_t m, int nq, uint32_t nbits,
+                                                  const PackedSeeds& ps, int k, uint64_t H,
+                                                  const uint32_t* __restrict__ colmask) {
+  const uint32_t* cm = colmask + p.l0 * 32;  // colmask[l0][c]
+  uint32_t bits = 0;
+  int j0 = 0;
+  int ls = (int)p.l0;  // last digit at j0
+  uint32_t x = p.x;
+  uint64_t Q = p.Q;
+  while (j0 < (int)nbits) {
+    // segment [j0, j1): rows x .. M-1 of block Q
+    const int rowstart = j0 - ls;  // position of the first row's start
+    const int j1 = min((int)nbits, rowstart + (int)(m - x) * (int)m);
+    for (int s = 0; s < k; ++s) {
+      if (((((Q | H) - ps.q[s]) & H) == H)) {
+        const uint32_t sx = ps.xl[s] >> 8, sl = ps.xl[s] & 0xFFu;
+        const int jx = sx > x ? rowstart + (int)(sx - x) * (int)m : j0;
+        bits |= __ldg(cm + sl) & range_bits(jx, j1);
+      }
+    }
+    // next block: Q + 1, x = 0, last digit 0
+    j0 = j1;
+    ls = 0;
+    x = 0;
+    Q = q_add(Q, 1, m, nq);
+  }
+  return bits & range_bits(0, (int)nbits);
+}
+
+// Noise pass over a truth word: re-verdicts every configuration whose verdict
+// the router noise can change (router.cpp:50-57).
+template <int NT>
+__device__ __forceinline__ uint32_t noisy_word(const SpaceDev& sp, uint32_t i0, uint32_t nbits,
+                                               uint32_t truth, const RouterDev& rt, uint64_t P) {
+  constexpr int kN = DigitsT<NT>::kN;
+  const int n = NT > 0 ? NT : sp.n;
+  const uint32_t m = (uint32_t)sp.m;
+  const uint32_t valid = range_bits(0, (int)nbits);
+  const uint32_t need = ((rt.t_fn > 0) ? truth : 0u) | ((rt.t_fp > 0) ? ~truth : 0u);
+  uint32_t out = truth & ~need;
+  if (!(need & valid)) return out & valid;
+  uint32_t d[kN];
+  decode<NT>(sp, i0, d);
+  uint64_t h[kN];  // h[a] = hash after digits 0..a-1, valid for a < hvalid
+  h[0] = kHashIV;
+  int hvalid = 1;
+  uint64_t s1 = 0;
+  bool s1_ok = false;
+  uint32_t dl = d[n - 1];
+  for (uint32_t j = 0; j < nbits; ++j) {
+    if ((need >> j) & 1u) {
+      if (!s1_ok) {
+#pragma unroll
+        for (int a = 0; a < kN - 1; ++a) {
+          if (NT == 0 && a >= n - 1) break;
+          if (a + 1 >= hvalid) h[a + 1] = absorb(absorb(kMixIV, h[a]), d[a]);
+        }
+        hvalid = n;
+        s1 = absorb(kMixIV, h[n - 1]);
+        s1_ok = true;
+      }
+      const uint64_t key = absorb(P, absorb(s1, dl)) >> 11;
+      const bool t = (truth >> j) & 1u;
+      const bool v = t ? key >= rt.t_fn : key < rt.t_fp;
+      out |= (uint32_t)v << j;
+    }
+    if (++dl == m) {
+      dl = 0;
+      if (j + 1 < nbits) {
+        int changed = n - 1;
+        bool carry = true;
+#pragma unroll
+        for (int a = kN - 2; a >= 0; --a) {
+          if (NT == 0 && a >= n - 1) continue;
+          if (carry) {
+            changed = a;
+            if (++d[a] == m) d[a] = 0;
+            else carry = false;
+          }
+        }
+        if (changed + 1 < hvalid) hvalid = changed + 1;
+        s1_ok = false;
+      }
+    }
+  }
+  return out & valid;
+}
+
+struct ScoreArgs {
+  SpaceDev sp;
+  TruthDev t;
+  RouterDev rt;
+  uint64_t begin, end;
+  uint32_t W;        // words per request
+  uint32_t C;        // warp-tasks per request
+  uint64_t div_c;    // ceil(2^64 / C)
+  int R;
+  uint32_t flags;
+  uint64_t H;        // SWAR high-bit mask over N-2 bytes
+  int path2d;        // 2-D mask path available for this space
+  const uint32_t* colmask;
+  uint32_t* bitmap;  // [R * W]
+  uint32_t* task_counts;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
+  __shared__ PackedSeeds s_seeds[kWarpsPerBlock];
+  __shared__ uint32_t s_tr[kWarpsPerBlock][32][33];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t task = blockIdx.x * kWarpsPerBlock + wid;
+  if ((uint64_t)task >= (uint64_t)a.R * a.C) return;
+  // exact task / C (ceil(2^64/C) magic; C == 1 has no 64-bit magic)
+  const uint32_t r = a.C == 1 ? task : (uint32_t)__umul64hi(task, a.div_c);
+  const uint32_t c = task - r * a.C;
+  const int n = NT > 0 ? NT : a.sp.n;
+  const int s0 = __ldg(a.t.seed_ptr + r), s1 = __ldg(a.t.seed_ptr + r + 1);
+  const int k = s1 - s0;
+  const uint8_t* seeds = a.t.seeds + (size_t)s0 * n;
+  const bool fast = a.path2d && k <= kMaxFastSeeds;
+  if (fast) {
+    if (lane < k) {
+      const uint8_t* sd = seeds + (size_t)lane * n;
+      uint64_t q = 0;
+      for (int b = 0; b < n - 2; ++b) q |= (uint64_t)__ldg(sd + n - 3 - b) << (8 * b);
+      s_seeds[wid].q[lane] = q;
+      s_seeds[wid].xl[lane] = ((uint32_t)__ldg(sd + n - 2) << 8) | __ldg(sd + n - 1);
+    }
+    __syncwarp();
+  }
+  const int r0 = __ldg(a.t.removed_ptr + r), r1 = __ldg(a.t.removed_ptr + r + 1);
+  uint64_t P = 0;
+  if (a.rt.kind == AG_ROUTER_NOISY)
+    P = absorb(absorb(absorb(kMixIV, a.rt.noise_seed), kRouterSalt), __ldg(a.t.request_ids + r));
+  const uint64_t top = a.sp.size - 1;
+  const uint32_t m = (uint32_t)a.sp.m;
+  const int nq = a.sp.n - 2;
+  uint32_t cnt = 0;
+  // lane L owns the 32 consecutive words wbeg + 32L .. +31 (digit state is
+  // carried, no division per word); words go through a padded shared-memory
+  // transpose so the bitmap stores stay coalesced.
+  const uint32_t wbeg = c * kTaskWords;
+  const uint32_t wend = min(a.W, wbeg + kTaskWords);
+  const uint32_t wl = wbeg + 32u * lane;
+  const uint32_t i0s = (uint32_t)(a.begin + (uint64_t)wl * 32);  // < 2^32 when wl < wend
+  // all 32 words of this lane are full and inside [begin, end)
+  const bool full = (uint64_t)i0s + 1024 <= a.end && wl + 32 <= wend;
+  const bool extras = (r1 > r0) || a.rt.kind == AG_ROUTER_NOISY || (a.flags & AG_FORCE_TOP);
+  if (fast && full && !extras) {
+    // hot path: oracle router, no removals, 32 full words
+    WordPos pos = word_pos(a.sp, i0s);
+#pragma unroll 4
+    for (uint32_t it = 0; it < 32; ++it) {
+      const uint32_t word = truth_word_2d(pos, m, nq, 32u, s_seeds[wid], k, a.H, a.colmask);
+      advance32(pos, m, a.sp.div_m, nq);
+      cnt += __popc(word);
+      s_tr[wid][lane][it] = word;
+    }
+  } else {
+    WordPos pos{};
+    if (fast && wl < wend) pos = word_pos(a.sp, i0s);
+    uint64_t i0 = a.begin + (uint64_t)wl * 32;
+    for (uint32_t it = 0; it < 32; ++it, i0 += 32) {
+      const uint32_t w = wl + it;
+      uint32_t word = 0;
+      if (w < wend) {
+        const uint32_t nbits = (uint32_t)min((uint64_t)32, a.end - i0);
+        if (fast) {
+          word = truth_word_2d(pos, m, nq, nbits, s_seeds[wid], k, a.H, a.colmask);
+          advance32(pos, m, a.sp.div_m, nq);
+        } else {
+          word = truth_word_generic<NT>(a.sp, (uint32_t)i0, nbits, seeds, k);
+        }
+        // removed configurations (AccurateSet::removed, accuracy.cpp:117-119)
+        for (int i = r0; i < r1; ++i) {
+          const uint64_t x = __ldg(a.t.removed + i);
+          if (x >= i0 && x < i0 + nbits) word &= ~(1u << (uint32_t)(x - i0));
+        }
+        if (a.rt.kind == AG_ROUTER_NOISY)
+          word = noisy_word<NT>(a.sp, (uint32_t)i0, nbits, word, a.rt, P);
+        if ((a.flags & AG_FORCE_TOP) && top >= i0 && top < i0 + nbits)
+          word |= 1u << (uint32_t)(top - i0);
+        cnt += __popc(word);
+      }
+      s_tr[wid][lane][it] = word;
+    }
+  }
+  __syncwarp();
+  uint32_t* brow = a.bitmap + (size_t)r * a.W + wbeg;
+  const uint32_t nw = wend - wbeg;
+  for (uint32_t it = 0; it < 32; ++it) {
+    const uint32_t o = it * 32u + lane;  // word wbeg + o, owned by lane it
+    if (o < nw) brow[o] = s_tr[wid][it][lane];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if (lane == 0) a.task_counts[task] = cnt;
+}
+
+// K2a: one warp per request: exclusive scan of its task counts -> task
+// offsets (relative to the request), counts[r] = request total.
+__global__ void __launch_bounds__(kThreads)
+    k_chunk_scan(const uint32_t* __restrict__ task_counts, uint64_t* __restrict__ task_off,
+                 uint64_t* __restrict__ counts, uint32_t C, int R) {
+  const int lane = threadIdx.x & 31;
+  const int r = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if (r >= R) return;
+  const uint32_t* in = task_counts + (size_t)r * C;
+  uint64_t* out = task_off + (size_t)r * C;
+  uint64_t carry = 0;
+  for (uint32_t base = 0; base < C; base += 32) {
+    const uint32_t i = base + lane;
+    const uint64_t v = i < C ? in[i] : 0u;
+    uint64_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < C) out[i] = carry + (x - v);
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) counts[r] = carry;
+}
+
+// K2b: exclusive scan over requests -> offsets[R+1], overflow flag.  One
+// block; each thread owns a contiguous run of requests.
+__global__ void __launch_bounds__(1024)
+    k_request_scan(const uint64_t* __restrict__ counts, uint64_t* __restrict__ offsets, int R,
+                   uint64_t capacity, uint32_t* __restrict__ overflow) {
+  __shared__ uint64_t warp_sums[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int per = (R + 1023) / 1024;
+  const int lo = min(R, (int)threadIdx.x * per), hi = min(R, lo + per);
+  uint64_t local = 0;
+  for (int i = lo; i < hi; ++i) local += counts[i];
+  uint64_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t v = warp_sums[lane], z = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    warp_sums[lane] = z - v;  // exclusive warp prefix
+  }
+  __syncthreads();
+  uint64_t run = warp_sums[wid] + x - local;
+  for (int i = lo; i < hi; ++i) {
+    offsets[i] = run;
+    run += counts[i];
+  }
+  if (hi == R && lo < hi) {
+    offsets[R] = run;
+    if (overflow) *overflow = run > capacity ? 1u : 0u;
+  }
+}
+
+// K3: stream compaction of the verdict bitmap into canonical-order indices.
+// Each iteration the warp loads 32 words (coalesced), scans their popcounts,
+// then walks the non-empty words: the 32 lanes test the 32 bits and the set
+// lanes store their index at prefix(word) + popc(word & lanemask_lt) -- one
+// contiguous run per store instruction, no shared memory.
+__global__ void __launch_bounds__(kThreads)
+    k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ task_off,
+                    const uint64_t* __restrict__ offsets, uint64_t begin, uint32_t W, uint32_t C,
+                    uint64_t div_c, int R, uint32_t* __restrict__ indices, uint64_t capacity) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
+  if ((uint64_t)task >= (uint64_t)R * C) return;
+  const uint32_t r = C == 1 ? task : (uint32_t)__umul64hi(task, div_c);
+  const uint32_t c = task - r * C;
+  uint64_t base = __ldg(offsets + r) + __ldg(task_off + task);
+  const uint32_t lt = (1u << lane) - 1u;
+  const uint32_t* brow = bitmap + (size_t)r * W;
+  const uint32_t wbeg = c * kTaskWords;
+  const uint32_t wend = min(W, wbeg + kTaskWords);
+  uint32_t next = wbeg + lane < wend ? __ldg(brow + wbeg + lane) : 0u;
+  for (uint32_t wb = wbeg; wb < wend; wb += 32) {
+    const uint32_t word = next;  // software-pipelined: fetch the next 32 words now
+    const uint32_t wn = wb + 32 + lane;
+    next = wn < wend ? __ldg(brow + wn) : 0u;
+    uint32_t nz = __ballot_sync(0xffffffffu, word != 0);
+    if (!nz) continue;
+    const uint32_t pc = __popc(word);
+    uint32_t x = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    const uint32_t excl = x - pc;
+    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+    const uint32_t ibase = (uint32_t)(begin + (uint64_t)wb * 32) + (uint32_t)lane;
+    const uint64_t out = (uint64_t)(indices + base);
+    if (base + total <= capacity) {
+      const uint32_t bit = 1u << lane;
+      while (nz) {
+        // any order works: every word owns a precomputed output range
+        const int src = 31 - __clz(nz);
+        nz ^= 1u << src;
+        const uint32_t ww = __shfl_sync(0xffffffffu, word, src);
+        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
+        const uint32_t rank = pre + __popc(ww & lt);
+        const uint32_t val = ibase + ((uint32_t)src << 5);
+        // predicated store at out + 4*rank (one wide mad), no branch
+        asm volatile(
+            "{ .reg .pred p; .reg .u64 a; setp.ne.u32 p, %3, 0;"
+            " mad.wide.u32 a, %1, 4, %0; @p st.global.u32 [a], %2; }" ::"l"(out),
+            "r"(rank), "r"(val), "r"(ww & bit)
+            : "memory");
+      }
+    } else {
+      while (nz) {
+        const int src = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t ww = __shfl_sync(0xffffffffu, word, src);
+        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
+        const uint64_t o = base + pre + __popc(ww & lt);
+        if (((ww >> lane) & 1u) && o < capacity) indices[o] = ibase + (uint32_t)src * 32u;
+      }
+    }
+    base += total;
+  }
+}
+
+template <int NT>
+void launch_score(dim3 g, cudaStream_t s, const ScoreArgs& a) {
+  k_route_score<NT><<<g, kThreads, 0, s>>>(a);
+}
+
+typedef void (*score_fn)(dim3, cudaStream_t, const ScoreArgs&);
+
+score_fn pick_score(int n) {
+  switch (n) {
+    case 1: return launch_score<1>;
+    case 2: return launch_score<2>;
+    case 3: return launch_score<3>;
+    case 4: return launch_score<4>;
+    case 5: return launch_score<5>;
+    case 6: return launch_score<6>;
+    case 7: return launch_score<7>;
+    case 8: return launch_score<8>;
+    case 9: return launch_score<9>;
+    case 10: return launch_score<10>;
+    case 11: return launch_score<11>;
+    case 12: return launch_score<12>;
+    default: return launch_score<0>;
+  }
+}
+
+// ceil(2^64 / d) for exact u32 division via __umul64hi; d <= 1 is handled
+// by the callers (C == 1 means task == request)
+inline uint64_t magic_div(uint32_t d) { return d > 1 ? (~0ULL) / (uint64_t)d + 1 : 0; }
+
+// colmask[l0][c] = positions j in 0..31 with (l0 + j) mod M >= c
+int ensure_colmask(ag_ctx* ctx) {
+  const int m = ctx->space->m;
+  if (ctx->colmask.bytes >= 32 * 32 * 4 && ctx->colmask_m == m) return AG_OK;
+  std::vector<uint32_t> h(32 * 32, 0);
+  for (int l0 = 0; l0 < m && l0 < 32; ++l0)
+    for (int c = 0; c < m && c < 32; ++c) {
+      uint32_t bits = 0;
+      for (int j = 0; j < 32; ++j)
+        if ((l0 + j) % m >= c) bits |= 1u << j;
+      h[l0 * 32 + c] = bits;
+    }
+  int rc = ctx->colmask.ensure(h.size() * 4);
+  if (rc) return rc;
+  AG_CUDA(cudaMemcpy(ctx->colmask.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+  ctx->colmask_m = m;
+  return AG_OK;
+}
+
+}  // namespace
+
+int make_router(const ag_router* r, RouterDev* out) {
+  if (!r) return fail(AG_ERR_VALIDATION, "router is null");
+  RouterDev d{};
+  d.kind = r->kind;
+  d.noise_seed = r->noise_seed;
+  if (r->eval_latency < 0) return fail(AG_ERR_VALIDATION, "router eval latency < 0");
+  if (r->kind == AG_ROUTER_NOISY) {
+    // NoisyRouter ctor check (router.cpp:41-48); NaN passes it there, and a
+    // NaN rate makes the corresponding comparison always false.
+    if (r->fp < 0 || r->fp > 1 || r->fn < 0 || r->fn > 1)
+      return fail(AG_ERR_VALIDATION, "router error rates outside [0, 1]");
+    d.t_fn = std::isnan(r->fn) ? ~0ULL : (uint64_t)std::ceil(r->fn * 0x1.0p53);
+    d.t_fp = std::isnan(r->fp) ? 0ULL : (uint64_t)std::ceil(r->fp * 0x1.0p53);
+  } else if (r->kind != AG_ROUTER_ORACLE) {
+    return fail(AG_ERR_VALIDATION, "unknown router kind");
+  }
+  *out = d;
+  return AG_OK;
+}
+
+int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t begin,
+                    uint64_t end, uint32_t flags, const ag_route_out* out) {
+  const ag_space* sp = ctx->space;
+  if (!t || !out) return fail(AG_ERR_VALIDATION, "null truth/out");
+  if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N <= 2^32 and N <= 32");
+  if (begin > end || end > sp->size) return fail(AG_ERR_VALIDATION, "configuration index out of range");
+  if (t->n_requests < 0) return fail(AG_ERR_VALIDATION, "negative request count");
+  RouterDev rt;
+  int rc = make_router(r, &rt);
+  if (rc) return rc;
+  const int R = t->n_requests;
+  cudaStream_t s = ctx->stream;
+  if (R == 0) {
+    if (out->offsets) AG_CUDA(cudaMemsetAsync(out->offsets, 0, 8, s));
+    if (out->overflow) AG_CUDA(cudaMemsetAsync(out->overflow, 0, 4, s));
+    return AG_OK;
+  }
+  if (!out->counts) return fail(AG_ERR_VALIDATION, "counts output is required");
+  const uint64_t range = end - begin;
+  const uint32_t W = (uint32_t)((range + 31) / 32);
+  const uint32_t C = (W + kTaskWords - 1) / kTaskWords;
+  const uint64_t ntasks = (uint64_t)R * C;
+  if (ntasks >= (1ULL << 31)) return fail(AG_ERR_VALIDATION, "batch too large for one launch");
+
+  if ((rc = ctx->chunk_counts.ensure(ntasks * 4))) return rc;
+  if ((rc = ctx->chunk_off.ensure(ntasks * 8))) return rc;
+  if ((rc = ensure_colmask(ctx))) return rc;
+  uint32_t* bitmap = out->bitmap;
+  if (!bitmap) {
+    if ((rc = ctx->bitmap.ensure((size_t)R * W * 4 + 4))) return rc;
+    bitmap = (uint32_t*)ctx->bitmap.p;
+  }
+  uint64_t* offsets = out->offsets;
+  if (!offsets) {
+    if ((rc = ctx->offsets.ensure(((size_t)R + 1) * 8))) return rc;
+    offsets = (uint64_t*)ctx->offsets.p;
+  }
+  ScoreArgs a;
+  a.sp = sp->dev();
+  a.t = TruthDev{R, t->request_ids, t->seed_ptr, t->seeds, t->removed_ptr, t->removed};
+  a.rt = rt;
+  a.begin = begin;
+  a.end = end;
+  a.W = W;
+  a.C = C;
+  a.div_c = magic_div(C);
+  a.R = R;
+  a.flags = flags;
+  a.H = 0;
+  for (int b = 0; b < sp->n - 2 && b < 8; ++b) a.H |= 0x80ull << (8 * b);
+  a.path2d = (sp->n >= 2 && sp->n - 2 <= 8 && sp->m <= 32) ? 1 : 0;
+  a.colmask = (const uint32_t*)ctx->colmask.p;
+  a.bitmap = bitmap;
+  a.task_counts = (uint32_t*)ctx->chunk_counts.p;
+  const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  if (range > 0) {
+    {
+      Launch L(ctx, K_ROUTE_SCORE);
+      pick_score(sp->n)(grid, s, a);
+    }
+    {
+      Launch L(ctx, K_CHUNK_SCAN);
+      k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
+          (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C, R);
+    }
+  } else {
+    AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
+  }
+  {
+    Launch L(ctx, K_REQUEST_SCAN);
+    k_request_scan<<<1, 1024, 0, s>>>(out->counts, offsets, R,
+                                     out->indices ? out->capacity : ~0ULL, out->overflow);
+  }
+  if (out->indices && range > 0) {
+    Launch L(ctx, K_ROUTE_COMPACT);
+    k_route_compact<<<grid, kThreads, 0, s>>>(bitmap, (const uint64_t*)ctx->chunk_off.p, offsets,
+                                              begin, W, C, magic_div(C), R, out->indices,
+                                              out->capacity);
+  }
+  AG_CUDA(cudaGetLastError());
+  return AG_OK;
+}
+
+// Compaction pass alone, reusing the task offsets of the preceding
+// route_enumerate on this context (the host path's second phase).
+int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32_t* bitmap,
+                  const uint64_t* offsets, uint32_t* indices, uint64_t capacity) {
+  const uint64_t range = end - begin;
+  if (R == 0 || range == 0) return AG_OK;
+  const uint32_t W = (uint32_t)((range + 31) / 32);
+  const uint32_t C = (W + kTaskWords - 1) / kTaskWords;
+  const uint64_t ntasks = (uint64_t)R * C;
+  const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
+  Launch L(ctx, K_ROUTE_COMPACT);
+  k_route_compact<<<grid, kThreads, 0, ctx->stream>>>(bitmap, (const uint64_t*)ctx->chunk_off.p,
+                                                      offsets, begin, W, C, magic_div(C), R,
+                                                      indices, capacity);
+  AG_CUDA(cudaGetLastError());
+  return AG_OK;
+}
+
+}  // namespace agb
