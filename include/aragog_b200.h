@@ -158,6 +158,42 @@ int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* truth_host,
                             uint64_t* offsets, uint32_t* indices,
                             uint64_t capacity, uint64_t* total);
 
+/* ---- chain mode ---------------------------------------------------------- */
+typedef struct ag_predictor ag_predictor;
+
+/* ConfigPredictor(space, router, PredictorParams{chain_cap, exhaustive_limit})
+ * (include/aragog/predictor.h:70-103; src/predictor.cpp:107-131,158-163):
+ * builds the chain plan on the host once and uploads it.  chain_cap <= 0
+ * means 64; the plan covers the lattice when M^N <= exhaustive_limit. */
+int ag_predictor_create(ag_ctx* ctx, int chain_cap, uint64_t exhaustive_limit,
+                        ag_predictor** out);
+void ag_predictor_destroy(ag_predictor* p);
+/* ChainPlan (predictor.h:41-46): chains (host, optional) receives
+ * n_chains * chain_len canonical indices. */
+int ag_predictor_info(const ag_predictor* p, int32_t* n_chains,
+                      int32_t* chain_len, int32_t* exhaustive,
+                      int32_t* n_unique, uint64_t* chains);
+
+/* PredictionResult (predictor.h:75-83) for a batch, device pointers.
+ * viable: [R * viable_stride] canonical indices in canonical order (the
+ * ViableSet, always containing top); n_viable [R]; the rest optional. */
+typedef struct {
+  uint32_t* viable;
+  int32_t viable_stride; /* >= ag_predictor_info n_unique suffices */
+  int32_t* n_viable;
+  int32_t* search_evals;
+  int32_t* verify_evals;
+  double* router_time;
+  uint8_t* truncated;
+} ag_predict_out;
+
+/* ConfigPredictor::predict(request, budget) (predictor.cpp:165-262) for every
+ * request of the batch; budgets [R] device (seconds, may be +inf) or NULL to
+ * use budget_all.  router.eval_latency is the per-evaluation charge. */
+int ag_predict(ag_predictor* p, const ag_truth* truth_dev,
+               const ag_router* router, const double* budgets,
+               double budget_all, const ag_predict_out* out_dev);
+
 /* ======================================================================== *
  * Host-side input synthesis (reference generators; not on the hot path)     *
  * ======================================================================== */

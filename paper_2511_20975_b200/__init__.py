@@ -4,3 +4,4 @@ just-in-time scheduling, behind the C ABI in include/aragog_b200.h."""
 from ._capi import AgError, ValidationError, lib  # noqa: F401
 from .routing import (AccuracyBatch, ConfigSpace, Device, DeviceAccuracyBatch,  # noqa: F401
                       GenParams, NoisyRouter, OracleRouter, RouteResult, enumerate_members)
+from .predictor import ConfigPredictor, PredictionBatch  # noqa: F401,E402
