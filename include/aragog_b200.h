@@ -195,6 +195,94 @@ int ag_predict(ag_predictor* p, const ag_truth* truth_dev,
                double budget_all, const ag_predict_out* out_dev);
 
 /* ======================================================================== *
+ * Per-stage scheduling (hot path 2)                                         *
+ * ======================================================================== */
+
+/* Engine pools, EngineState (include/aragog/engine.h:38-53), host arrays. */
+typedef struct {
+  int32_t n_engines;
+  const int32_t* model;     /* [E] tier each pool serves */
+  const int32_t* slots;     /* [E] */
+  const int32_t* occupancy; /* [E] stages in flight */
+  const double* weight;     /* [E] utilization weight of one busy slot */
+} ag_engines;
+
+/* AssignmentTriple (scheduler.h:50-55) plus the session slot. */
+typedef struct {
+  int32_t request_index; /* index into the round's queue (container order) */
+  int32_t agent;         /* canonical position */
+  int32_t model;
+  int32_t slot;          /* session slot (ag_sched_*), -1 for ag_beam_schedule */
+  uint64_t request_id;
+} ag_triple;
+
+/* Assignment (scheduler.h:76-83); triples/occupancy returned separately. */
+typedef struct {
+  int32_t n_triples;
+  int32_t pad;
+  double utilization;
+  double flexibility;
+  int64_t skips;
+  uint64_t states_explored;
+} ag_assignment;
+
+/* StageState (request.h:24) */
+#define AG_STAGE_PENDING 0
+#define AG_STAGE_READY 1
+#define AG_STAGE_INFLIGHT 2
+#define AG_STAGE_DONE 3
+
+/* The round's vector<const Request*> (request.h:30-47) as host arrays:
+ * stages [R*N] by canonical position, viable CSR of canonical indices. */
+typedef struct {
+  int32_t n_requests;
+  const uint64_t* ids;       /* [R] */
+  const double* arrival;     /* [R] */
+  const uint8_t* stages;     /* [R*N] */
+  const int64_t* viable_ptr; /* [R+1] */
+  const uint32_t* viable;    /* [viable_ptr[R]] */
+} ag_queue;
+
+/* beam_schedule(queue, engines, {beam_width}) (scheduler.h:85-87,
+ * scheduler.cpp:289-378), stateless: uploads the queue, runs one round on
+ * the GPU, returns the Assignment.  triples [triples_cap], occupancy [E].
+ * Validation mirrors the reference (beam width < 1, > 32 pools, duplicate
+ * or negative tiers, a viable tier without a pool, an over-capacity pool);
+ * the GPU path additionally needs beam_width <= 32 and M <= 32. */
+int ag_beam_schedule(ag_ctx* ctx, const ag_queue* queue,
+                     const ag_engines* engines, int beam_width,
+                     ag_assignment* out, ag_triple* triples,
+                     int32_t triples_cap, int32_t* occupancy);
+
+/* Resident scheduling session: the in-flight Request objects live in HBM
+ * (viable lists, per-agent candidate masks and model histograms, ready
+ * masks); rounds read them in place and dispatch prunes them in place. */
+typedef struct ag_sched ag_sched;
+
+int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs,
+                    ag_sched** out);
+void ag_sched_destroy(ag_sched* s);
+/* Request::make for each row (request.cpp:24-50); the requests join the FIFO
+ * queue ordered by (arrival, id).  slots_out [R] receives their slots. */
+int ag_sched_add(ag_sched* s, const ag_queue* requests, int32_t* slots_out);
+/* the request leaves the session (finished); its slot is recycled */
+int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots);
+/* Request::mark_complete(agent) (request.cpp:88-107): done, successors whose
+ * predecessors are all done become ready. */
+int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent);
+/* One scheduling round over every session request with a ready stage, in
+ * FIFO order (Sim::on_round, simulation.cpp:300-318 -> beam_schedule). */
+int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width,
+                   ag_assignment* out, ag_triple* triples, int32_t triples_cap,
+                   int32_t* occupancy);
+/* Request::mark_dispatched for applied triples (request.cpp:70-86): prefix
+ * prune of the viable list in HBM, stage -> in flight. */
+int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied);
+/* read back one request's current viable list (host buffer) */
+int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap,
+                    int64_t* n);
+
+/* ======================================================================== *
  * Host-side input synthesis (reference generators; not on the hot path)     *
  * ======================================================================== */
 typedef struct {

@@ -1,0 +1,166 @@
+"""Per-stage scheduler: host mirror of beam_schedule / Request over the C ABI.
+
+Reference: include/aragog/scheduler.h:37-118, src/scheduler.cpp:29-454,
+include/aragog/request.h:30-67.  `beam_schedule` is the stateless drop-in
+(uploads the queue every call); `SchedSession` keeps the in-flight requests
+resident in HBM across rounds, as the simulator's event loop uses them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._capi import check, lib
+from .routing import Device, _ptr
+
+PENDING, READY, INFLIGHT, DONE = 0, 1, 2, 3
+
+
+class CEngines(C.Structure):
+    _fields_ = [("n_engines", C.c_int32), ("model", C.c_void_p), ("slots", C.c_void_p),
+                ("occupancy", C.c_void_p), ("weight", C.c_void_p)]
+
+
+class CTriple(C.Structure):
+    _fields_ = [("request_index", C.c_int32), ("agent", C.c_int32), ("model", C.c_int32),
+                ("slot", C.c_int32), ("request_id", C.c_uint64)]
+
+
+class CAssignment(C.Structure):
+    _fields_ = [("n_triples", C.c_int32), ("pad", C.c_int32), ("utilization", C.c_double),
+                ("flexibility", C.c_double), ("skips", C.c_int64), ("states_explored", C.c_uint64)]
+
+
+class CQueue(C.Structure):
+    _fields_ = [("n_requests", C.c_int32), ("ids", C.c_void_p), ("arrival", C.c_void_p),
+                ("stages", C.c_void_p), ("viable_ptr", C.c_void_p), ("viable", C.c_void_p)]
+
+
+@dataclass
+class Engines:
+    """vector<EngineState> (engine.h:38-53): one pool per tier."""
+    model: list
+    slots: list
+    occupancy: list
+    weight: list
+
+    def c(self):
+        self._arrs = [np.ascontiguousarray(self.model, np.int32),
+                      np.ascontiguousarray(self.slots, np.int32),
+                      np.ascontiguousarray(self.occupancy, np.int32),
+                      np.ascontiguousarray(self.weight, np.float64)]
+        return CEngines(len(self.model), *[_ptr(a) for a in self._arrs])
+
+
+@dataclass
+class Assignment:
+    """Assignment (scheduler.h:76-83); triples are (request_index, request_id,
+    agent, model) as in the reference, `slots` the session slots."""
+    triples: list
+    occupancy: list
+    utilization: float
+    flexibility: float
+    skips: int
+    states_explored: int
+    slots: list = field(default_factory=list)
+
+
+class Queue:
+    """The round's vector<const Request*> as flat host arrays."""
+
+    def __init__(self, n_agents, ids, arrival, stages, viable_lists):
+        self.n = n_agents
+        self.ids = np.ascontiguousarray(ids, np.uint64)
+        self.arrival = np.ascontiguousarray(arrival, np.float64)
+        self.stages = np.ascontiguousarray(np.asarray(stages, np.uint8).reshape(-1))
+        ptr = [0]
+        for v in viable_lists:
+            ptr.append(ptr[-1] + len(v))
+        self.viable_ptr = np.asarray(ptr, np.int64)
+        self.viable = np.ascontiguousarray(
+            np.concatenate([np.asarray(v, np.uint32) for v in viable_lists]) if ptr[-1] else
+            np.zeros(1, np.uint32))
+
+    def c(self):
+        return CQueue(len(self.ids), _ptr(self.ids), _ptr(self.arrival), _ptr(self.stages),
+                      _ptr(self.viable_ptr), _ptr(self.viable))
+
+
+def _unpack(res: CAssignment, trip, occ, E):
+    tr = [(trip[i].request_index, trip[i].request_id, trip[i].agent, trip[i].model)
+          for i in range(res.n_triples)]
+    return Assignment(tr, list(occ[:E]), res.utilization, res.flexibility, res.skips,
+                      res.states_explored, [trip[i].slot for i in range(res.n_triples)])
+
+
+def beam_schedule(device: Device, queue: Queue, engines: Engines, beam_width: int = 4) -> Assignment:
+    """beam_schedule(queue, engines, {beam_width}) (scheduler.cpp:289-378)."""
+    cap = max(1, int(sum(max(0, s - o) for s, o in zip(engines.slots, engines.occupancy))) + 1)
+    trip = (CTriple * cap)()
+    occ = np.zeros(max(1, len(engines.model)), np.int32)
+    res = CAssignment()
+    q, e = queue.c(), engines.c()
+    check(lib().ag_beam_schedule(device.handle, C.byref(q), C.byref(e), beam_width,
+                                 C.byref(res), trip, cap, C.c_void_p(_ptr(occ))))
+    return _unpack(res, trip, occ, len(engines.model))
+
+
+class SchedSession:
+    """Resident requests (ag_sched): add -> round -> dispatch -> complete."""
+
+    def __init__(self, device: Device, max_requests: int, max_configs: int):
+        self.device = device
+        h = C.c_void_p()
+        check(lib().ag_sched_create(device.handle, max_requests, C.c_uint64(max_configs), C.byref(h)))
+        self._h = h
+        self._trip = None
+
+    def add(self, queue: Queue) -> np.ndarray:
+        """Request::make for each row; returns their slots."""
+        slots = np.zeros(max(1, len(queue.ids)), np.int32)
+        q = queue.c()
+        check(lib().ag_sched_add(self._h, C.byref(q), C.c_void_p(_ptr(slots))))
+        return slots[: len(queue.ids)]
+
+    def remove(self, slots):
+        s = np.ascontiguousarray(slots, np.int32)
+        check(lib().ag_sched_remove(self._h, len(s), C.c_void_p(_ptr(s))))
+
+    def complete(self, slot: int, agent: int):
+        """Request::mark_complete (request.cpp:88-107)."""
+        check(lib().ag_sched_complete(self._h, int(slot), int(agent)))
+
+    def round(self, engines: Engines, beam_width: int = 4) -> Assignment:
+        cap = max(1, int(sum(max(0, s - o) for s, o in zip(engines.slots, engines.occupancy))) + 1)
+        if self._trip is None or len(self._trip) < cap:
+            self._trip = (CTriple * max(cap, 256))()
+        occ = np.zeros(max(1, len(engines.model)), np.int32)
+        res = CAssignment()
+        e = engines.c()
+        check(lib().ag_sched_round(self._h, C.byref(e), beam_width, C.byref(res), self._trip,
+                                   len(self._trip), C.c_void_p(_ptr(occ))))
+        return _unpack(res, self._trip, occ, len(engines.model))
+
+    def dispatch(self, assignment: Assignment, keep=None):
+        """Request::mark_dispatched for the applied triples (default: all)."""
+        idx = range(len(assignment.triples)) if keep is None else keep
+        arr = (CTriple * max(1, len(idx)))()
+        for k, i in enumerate(idx):
+            qi, rid, a, m = assignment.triples[i]
+            arr[k] = CTriple(qi, a, m, assignment.slots[i], rid)
+        check(lib().ag_sched_dispatch(self._h, len(idx), arr))
+
+    def viable(self, slot: int) -> np.ndarray:
+        n = C.c_int64()
+        check(lib().ag_sched_viable(self._h, int(slot), None, 0, C.byref(n)))
+        out = np.zeros(max(1, n.value), np.uint32)
+        check(lib().ag_sched_viable(self._h, int(slot), C.c_void_p(_ptr(out)), len(out), C.byref(n)))
+        return out[: n.value]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().ag_sched_destroy(h)
+            self._h = None
