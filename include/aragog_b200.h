@@ -278,6 +278,11 @@ int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width,
 /* Request::mark_dispatched for applied triples (request.cpp:70-86): prefix
  * prune of the viable list in HBM, stage -> in flight. */
 int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied);
+/* diagnostics: device timestamps (ns) of the last round's phases:
+ * start, context built, candidates compacted, walk done, finalized */
+int ag_sched_round_timing(ag_sched* s, uint64_t* ns5);
+/* host wall time (us) of the last ag_sched_round call, entry to return */
+double ag_sched_last_round_us(const ag_sched* s);
 /* read back one request's current viable list (host buffer) */
 int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap,
                     int64_t* n);

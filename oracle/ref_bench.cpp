@@ -19,6 +19,8 @@
 //       serial per round).
 
 #include <algorithm>
+#include <array>
+#include <numeric>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -29,6 +31,7 @@
 #include <vector>
 
 #include "aragog/accuracy.h"
+#include "aragog/engine.h"
 #include "aragog/metrics.h"
 #include "aragog/predictor.h"
 #include "aragog/request.h"
@@ -126,6 +129,124 @@ int run_route(int n, int m, std::size_t requests, bool noisy, int threads,
   return 0;
 }
 
+// ---------------------------------------------------------------- config 3
+// The per-stage scheduling workload, identical to
+// paper_2511_20975_b200/workloads.py:
+//   * requests id = 0.. from generate_accurate_set(chain 5 x 8, defaults,
+//     seed, id); viable = ConfigPredictor::predict(id, inf) (oracle router)
+//     or, with exhaustive=1, the full accurate set;
+//   * request id arrives at id * 0.01 and is advanced k = mix({12345, id}) % 5
+//     stages, stage a choosing candidate_models(a)[mix({12345, id, a}) % #];
+//   * 8 pools x 32 slots; round r frees F = {1, 8, 64}[mix({seed, r}) % 3]
+//     slots: all pools full, then F draws e = mix({seed, r, j}) % 8 decrement
+//     a pool that is not empty;
+//   * every assigned stage dispatches (prefix prune) and completes at once;
+//     a finished request is replaced by the next id (steady in-flight count).
+// Times beam_schedule per round on one core (p50/p99) and hashes decisions.
+int run_sched(std::size_t inflight, int beam, int rounds, std::uint64_t seed, bool exhaustive) {
+  const int n = 5, m = 8;
+  WorkflowGraph g = chain_graph(n);
+  ModelCatalog cat = geometric_catalog(m);
+  ConfigSpace space(g, cat);
+  AccuracyGenParams ap;
+  OracleRouter* router = nullptr;
+  std::vector<AccurateSet> sets;
+  const std::size_t reserve = inflight + (std::size_t)rounds * 64 + 16;
+  sets.reserve(reserve);
+  for (std::size_t i = 0; i < reserve; ++i) sets.push_back(generate_accurate_set(space, ap, seed, i));
+  AccuracyTable table(space, sets);
+  router = new OracleRouter(table, 0.002);
+  ConfigPredictor predictor(space, *router);
+  auto make_request = [&](std::size_t id) {
+    std::vector<Configuration> viable;
+    if (exhaustive) {
+      for (std::uint64_t k = 0; k < space.size(); ++k) {
+        Configuration c = space.at_index(k);
+        if (table.accurate(id, c)) viable.push_back(std::move(c));
+      }
+    } else {
+      viable = predictor.predict(id, std::numeric_limits<double>::infinity()).viable.configs;
+    }
+    Request r = Request::make(id, (double)id * 0.01, g, std::move(viable));
+    const int k = (int)(rng::mix({12345ULL, (std::uint64_t)id}) % (std::uint64_t)n);
+    for (int a = 0; a < k; ++a) {
+      std::vector<int> cands = r.candidate_models(a);
+      const int mdl = cands[rng::mix({12345ULL, (std::uint64_t)id, (std::uint64_t)a}) % cands.size()];
+      r.mark_dispatched(a, mdl, 0.0);
+      r.mark_complete(a, 0.0);
+    }
+    return r;
+  };
+  std::vector<Request> live;  // FIFO order (ids increase with arrival)
+  live.reserve(inflight);
+  std::size_t next_id = 0;
+  while (live.size() < inflight) {
+    Request r = make_request(next_id++);
+    if (!r.finished()) live.push_back(std::move(r));
+  }
+  std::vector<double> lat_us;
+  std::uint64_t hash = 0x9e3779b97f4a7c15ULL;
+  std::uint64_t assigned = 0;
+  for (int rd = 0; rd < rounds; ++rd) {
+    const int F = std::array<int, 3>{1, 8, 64}[rng::mix({seed, (std::uint64_t)rd}) % 3];
+    std::vector<EngineState> engines(8);
+    for (int e = 0; e < 8; ++e) {
+      engines[e].model = e;
+      engines[e].slots = 32;
+      engines[e].weight = cat.at(e).slot_throughput;
+    }
+    std::vector<int> occ(8, 32);
+    for (int j = 0; j < F; ++j) {
+      const int e = (int)(rng::mix({seed, (std::uint64_t)rd, (std::uint64_t)j}) % 8);
+      if (occ[e] > 0) --occ[e];
+    }
+    for (int e = 0; e < 8; ++e)
+      for (int b = 0; b < occ[e]; ++b) engines[e].in_flight.push_back({999999, 0, 1e18});
+    std::vector<const Request*> queue;
+    std::vector<Request*> mut;
+    for (Request& r : live)
+      if (!r.ready_agents().empty()) {
+        queue.push_back(&r);
+        mut.push_back(&r);
+      }
+    auto t0 = Clock::now();
+    Assignment a = beam_schedule(queue, engines, SchedulerParams{beam});
+    auto t1 = Clock::now();
+    lat_us.push_back(secs(t0, t1) * 1e6);
+    for (const AssignmentTriple& t : a.triples) {
+      hash = rng::mix({hash, (std::uint64_t)t.request_index, t.request, (std::uint64_t)t.agent,
+                       (std::uint64_t)t.model});
+      ++assigned;
+    }
+    hash = rng::mix({hash, (std::uint64_t)(a.utilization * 1e6), a.states_explored,
+                     (std::uint64_t)a.skips});
+    ApplyOutcome out = apply_assignment(a, mut, engines, 0.0,
+                                        [](RequestId, int, int) { return 1.0; });
+    for (const AssignmentTriple& t : out.applied) mut[t.request_index]->mark_complete(t.agent, 0.0);
+    // replace finished requests, keeping FIFO order (new ids arrive last)
+    std::vector<Request> keep;
+    keep.reserve(live.size());
+    for (Request& r : live)
+      if (!r.finished()) keep.push_back(std::move(r));
+    live = std::move(keep);
+    while (live.size() < inflight) {
+      Request r = make_request(next_id++);
+      if (!r.finished()) live.push_back(std::move(r));
+    }
+  }
+  std::vector<double> s = lat_us;
+  std::sort(s.begin(), s.end());
+  auto pct = [&](double p) { return s[std::min(s.size() - 1, (std::size_t)(p * (double)s.size()))]; };
+  std::printf(
+      "{\"mode\":\"sched\",\"inflight\":%zu,\"beam\":%d,\"rounds\":%d,\"exhaustive\":%d,"
+      "\"p50_us\":%.3f,\"p99_us\":%.3f,\"mean_us\":%.3f,\"assigned\":%llu,\"hash\":\"%016llx\"}\n",
+      inflight, beam, rounds, exhaustive ? 1 : 0, pct(0.5), pct(0.99),
+      std::accumulate(s.begin(), s.end(), 0.0) / (double)s.size(),
+      (unsigned long long)assigned, (unsigned long long)hash);
+  delete router;
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -135,6 +256,11 @@ int main(int argc, char** argv) {
   }
   std::string mode = argv[1];
   try {
+    if (mode == "sched" && argc >= 7) {
+      return run_sched(static_cast<std::size_t>(std::atoll(argv[2])), std::atoi(argv[3]),
+                       std::atoi(argv[4]), static_cast<std::uint64_t>(std::atoll(argv[5])),
+                       std::atoi(argv[6]) != 0);
+    }
     if ((mode == "route" || mode == "predict") && argc >= 8) {
       return run_route(std::atoi(argv[2]), std::atoi(argv[3]),
                        static_cast<std::size_t>(std::atoll(argv[4])),

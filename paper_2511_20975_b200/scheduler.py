@@ -152,6 +152,21 @@ class SchedSession:
             arr[k] = CTriple(qi, a, m, assignment.slots[i], rid)
         check(lib().ag_sched_dispatch(self._h, len(idx), arr))
 
+    def round_timing(self):
+        """Device phase durations (us) of the last round: context, candidates,
+        walk, finalize."""
+        t = np.zeros(13, np.uint64)
+        check(lib().ag_sched_round_timing(self._h, C.c_void_p(_ptr(t))))
+        self.walk_cycles = t[5:9].astype(np.float64)
+        self.ctx_cycles = t[9:13].astype(np.float64)
+        return np.diff(t[:5].astype(np.float64)) / 1e3
+
+    def last_round_us(self) -> float:
+        """Host wall time of the last round inside the C ABI call."""
+        f = lib().ag_sched_last_round_us
+        f.restype = C.c_double
+        return float(f(self._h))
+
     def viable(self, slot: int) -> np.ndarray:
         n = C.c_int64()
         check(lib().ag_sched_viable(self._h, int(slot), None, 0, C.byref(n)))
