@@ -287,6 +287,37 @@ double ag_sched_last_round_us(const ag_sched* s);
 int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap,
                     int64_t* n);
 
+/* ---- runtime-cost re-cost + argmin -------------------------------------- */
+#define AG_POLICY_PER_INPUT_STATIC 2       /* PolicyKind::kPerInputStatic */
+#define AG_POLICY_PER_INPUT_RUNTIME_COST 3 /* PolicyKind::kPerInputRuntimeCost */
+
+/* RuntimeCostContext (include/aragog/workload.h:64-69), host arrays over
+ * n_tiers model tiers; mean[m] = ServiceTimeModel::mean(m) (engine.cpp:62-65),
+ * computed by the caller's libm exactly as the reference does. */
+typedef struct {
+  int32_t n_tiers;
+  const int32_t* occupancy;
+  const int32_t* queued_ahead;
+  const int32_t* slots;
+  const double* mean;
+} ag_load;
+
+/* select_per_input_config(set, space, kind, &load) (workload.cpp:149-176) for
+ * a batch: members / offsets are the device CSR of each request's accurate
+ * set (e.g. ag_route_enumerate's indices); chosen [R] (device) receives the
+ * canonical index, est [R] (device, optional) its estimate_completion.
+ * Static: minimum (static cost, index).  Runtime: minimum (estimate, static
+ * cost, index), the reference's strict '<' scan over the cost-sorted list. */
+int ag_select_per_input(ag_ctx* ctx, const uint32_t* members,
+                        const uint64_t* offsets, int32_t n_requests,
+                        int32_t kind, const ag_load* load, uint32_t* chosen,
+                        double* est);
+
+/* snapshot_load's queued_ahead (simulation.cpp:194-213): per model tier, the
+ * number of ready (request, agent) pairs of the session whose candidate set
+ * contains the tier.  out [M] host. */
+int ag_sched_queued_ahead(ag_sched* s, int32_t* out);
+
 /* ======================================================================== *
  * Host-side input synthesis (reference generators; not on the hot path)     *
  * ======================================================================== */

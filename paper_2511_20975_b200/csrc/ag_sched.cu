@@ -1044,6 +1044,30 @@ __global__ void __launch_bounds__(256) k_sched_prune(PruneArgs A) {
   if (tid == 0) A.nviable[s] = len;
 }
 
+// snapshot_load's queued_ahead (simulation.cpp:194-213): per tier, ready
+// pairs whose candidate models include it.  Dead slots have ready == 0.
+__global__ void __launch_bounds__(256)
+    k_queued_ahead(const int32_t* __restrict__ order, int Q, const uint64_t* __restrict__ ready,
+                   const uint32_t* __restrict__ cand, int N, int M, int n_upd,
+                   const int32_t* __restrict__ upd_slot, const uint64_t* __restrict__ upd_mask,
+                   uint32_t* __restrict__ out) {
+  __shared__ uint32_t h[32];
+  if (threadIdx.x < 32) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < Q; p += gridDim.x * blockDim.x) {
+    const int s = order[p];
+    uint64_t r = ready[s];
+    for (int i = 0; i < n_upd; ++i)  // pending host-side updates win
+      if (upd_slot[i] == s) r = upd_mask[i];
+    for (uint64_t b = r; b; b &= b - 1) {
+      const int a = __ffsll((long long)b) - 1;
+      for (uint32_t c = cand[(size_t)s * N + a]; c; c &= c - 1) atomicAdd(&h[__ffs(c) - 1], 1u);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < M) atomicAdd(out + threadIdx.x, h[threadIdx.x]);
+}
+
 }  // namespace
 }  // namespace agb
 
@@ -1075,7 +1099,7 @@ struct ag_sched {
   double last_round_us = 0.0;
   // device
   agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx;
-  agb::Scratch d_cpos, d_cmask, d_det, d_nodes, d_out, d_status, d_upd, d_gam;
+  agb::Scratch d_cpos, d_cmask, d_det, d_nodes, d_out, d_status, d_upd, d_gam, d_qa;
   // pinned host staging
   void* h_res = nullptr;
   size_t h_res_bytes = 0;
@@ -1570,6 +1594,40 @@ int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
     s->upd_mask.push_back(r);
   }
   return agb::launch_prune(s, g_slot, g_begin, g_am, nullptr);
+}
+
+int ag_sched_queued_ahead(ag_sched* s, int32_t* out) {
+  if (!s || !out) return fail(AG_ERR_VALIDATION, "null argument");
+  ag_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const int Q = (int)s->order.size();
+  const size_t nu = s->upd_slot.size();
+  int rc;
+  if ((rc = s->d_qa.ensure(4 * 32 + nu * 12 + 16))) return rc;
+  // the device order must be current; pending ready updates are passed along
+  if (Q > (int)s->dirty_from) {
+    AG_CUDA(cudaMemcpyAsync((int32_t*)s->d_order.p + s->dirty_from, s->order.data() + s->dirty_from,
+                            (Q - s->dirty_from) * 4, cudaMemcpyHostToDevice, st));
+    s->dirty_from = Q;
+  }
+  char* d = (char*)s->d_qa.p;
+  AG_CUDA(cudaMemsetAsync(d, 0, 4 * 32, st));
+  if (nu) {
+    AG_CUDA(cudaMemcpyAsync(d + 128, s->upd_mask.data(), nu * 8, cudaMemcpyHostToDevice, st));
+    AG_CUDA(cudaMemcpyAsync(d + 128 + nu * 8, s->upd_slot.data(), nu * 4, cudaMemcpyHostToDevice, st));
+  }
+  const int blocks = std::max(1, std::min(148, (Q + 255) / 256));
+  {
+    agb::Launch L(ctx, agb::K_SCHED_PREP);
+    agb::k_queued_ahead<<<blocks, 256, 0, st>>>(
+        (const int32_t*)s->d_order.p, Q, (const uint64_t*)s->d_ready.p, (const uint32_t*)s->d_cand.p,
+        s->N, s->M, (int)nu, (const int32_t*)(d + 128 + nu * 8), (const uint64_t*)(d + 128),
+        (uint32_t*)d);
+  }
+  AG_CUDA(cudaGetLastError());
+  AG_CUDA(cudaMemcpyAsync(out, d, 4 * (size_t)s->M, cudaMemcpyDeviceToHost, st));
+  AG_CUDA(cudaStreamSynchronize(st));
+  return AG_OK;
 }
 
 int ag_sched_round_timing(ag_sched* s, uint64_t* ns) {

@@ -179,3 +179,53 @@ class SchedSession:
         if h is not None and h.value:
             lib().ag_sched_destroy(h)
             self._h = None
+
+
+class CLoad(C.Structure):
+    _fields_ = [("n_tiers", C.c_int32), ("occupancy", C.c_void_p), ("queued_ahead", C.c_void_p),
+                ("slots", C.c_void_p), ("mean", C.c_void_p)]
+
+
+PER_INPUT_STATIC, PER_INPUT_RUNTIME_COST = 2, 3
+
+
+@dataclass
+class RuntimeCostContext:
+    """RuntimeCostContext (workload.h:64-69); mean[m] = ServiceTimeModel::mean."""
+    occupancy: list
+    queued_ahead: list
+    slots: list
+    mean: list
+
+    def c(self):
+        self._arrs = [np.ascontiguousarray(self.occupancy, np.int32),
+                      np.ascontiguousarray(self.queued_ahead, np.int32),
+                      np.ascontiguousarray(self.slots, np.int32),
+                      np.ascontiguousarray(self.mean, np.float64)]
+        return CLoad(len(self.slots), *[_ptr(a) for a in self._arrs])
+
+
+def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_COST, ctx=None):
+    """select_per_input_config for every request of a member CSR (device
+    tensors: members int32 [total], offsets int64 [R+1]).  Returns device
+    tensors (chosen canonical index, estimate)."""
+    import torch
+
+    R = offsets.numel() - 1
+    chosen = torch.zeros(max(R, 1), dtype=torch.int32, device=device.torch_device)
+    est = torch.zeros(max(R, 1), dtype=torch.float64, device=device.torch_device)
+    load = ctx.c() if ctx is not None else None
+    check(lib().ag_select_per_input(device.handle, C.c_void_p(_ptr(members)), C.c_void_p(_ptr(offsets)),
+                                    R, kind, C.byref(load) if load is not None else None,
+                                    C.c_void_p(_ptr(chosen)), C.c_void_p(_ptr(est))))
+    return chosen[:R], est[:R]
+
+
+def _queued_ahead(self) -> list:
+    """snapshot_load's queued_ahead per model tier (simulation.cpp:194-213)."""
+    out = np.zeros(64, np.int32)
+    check(lib().ag_sched_queued_ahead(self._h, C.c_void_p(_ptr(out))))
+    return out[: self.device.space.m].tolist()
+
+
+SchedSession.queued_ahead = _queued_ahead
