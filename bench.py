@@ -1,19 +1,29 @@
 #!/usr/bin/env python
-"""bench.py -- Aragog hot paths on B200.
+"""bench.py -- Aragog's two hot paths on B200, through the C ABI.
 
-Headline (BASELINE.json metric "configs routed/sec ..."): enumerate-mode
-routing of BASELINE config 2 -- a 5-stage chain x 8 model tiers (32,768
-configurations per request), a 10k-request batch per GPU, oracle router --
-through the C ABI (libaragog_b200.so).  One step = route one batch:
-score every configuration, scan, stream-compact the accurate set.
+Headline (BASELINE.json metric "configs routed/sec and p50/p99 per-stage
+scheduling latency"):
+
+  * routing, BASELINE config 2: enumerate-mode routing of a 5-stage chain x 8
+    model tiers (32,768 configurations per request), a 10k-request batch per
+    GPU, oracle router.  One step = route one batch: score every
+    configuration, scan, stream-compact the accurate set.  `value` is
+    configurations routed per second over all GPUs (inputs resident in HBM);
+    `e2e` is the same through the host-buffer call with copies included.
+  * per-stage scheduling, BASELINE config 3: 10k in-flight requests resident
+    on the GPU, 8 pools x 32 slots, free slots per round drawn from {1, 8, 64},
+    beam width 4; p50/p99 of the decision latency of ag_sched_round (host
+    wall time inside the C ABI call: upload of pending updates, the round
+    kernel, download of the assignment).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N > 1 runs under torchrun, one process per GPU; requests are sharded (each
-rank routes its own 10k requests, no data-path collective: weak scaling);
-the timed region is bracketed by barrier + synchronize and the max over ranks
-is taken.  `--impl reference` times the reference's own CPU implementation
-(oracle/_ref/ref_bench, compiled from /root/reference) on the host cores.
+rank routes its own 10k requests, no data-path collective: weak scaling); the
+timed region is bracketed by barrier + synchronize and the max over ranks is
+taken.  Scheduling is a per-GPU latency (replicas only, reported by rank 0).
+`--impl reference` times the reference's own CPU implementation
+(oracle/_ref/ref_bench, compiled unmodified from /root/reference).
 """
 from __future__ import annotations
 
@@ -37,6 +47,7 @@ UNIT = "configs/s"
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 CPU_SAMPLE_REQUESTS = 1000
+SCHED_INFLIGHT, SCHED_BEAM = 10_000, 4
 
 
 def workload_config(n_gpus):
@@ -46,7 +57,10 @@ def workload_config(n_gpus):
             "configs_per_request": N_TIERS ** N_AGENTS, "seed": SEED,
             "accuracy_gen": "AccuracyGenParams{} (easy .6 / medium .3 / hard .1, base .5)",
             "parallelism": f"request-sharded x{n_gpus}",
-            "l2": "flushed before every timed step (256 MiB write)"}
+            "l2": "flushed before every timed step (256 MiB write)",
+            "sched_workload": f"config3: {SCHED_INFLIGHT} in-flight requests (chain 5x8, viable sets "
+                              "from chain-mode predict), 8 pools x 32 slots, free slots "
+                              f"{{1,8,64}} per round, beam {SCHED_BEAM}"}
 
 
 def dist_env():
@@ -57,36 +71,40 @@ def dist_env():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region."""
+    """nvidia-smi sampling (clocks and throttle reasons) while work runs."""
+
+    FIELDS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", f"--id={index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
-                stderr=subprocess.DEVNULL)
+                 "--format=csv,noheader,nounits", "-lms", "50", "-f", self.path],
+                stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
 
     def stop(self):
         if self.p is None:
             return None
+        time.sleep(0.15)
         self.p.terminate()
         self.p.wait()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        finally:
+            os.unlink(self.path)
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in rows:
             try:
                 sm.append(float(r[0]))
                 mx = float(r[1])
-                for nm, v in zip(names, r[3:7]):
+                for nm, v in zip(self.FIELDS, r[3:7]):
                     if v.strip().lower() == "active":
                         reasons.add(nm)
             except (ValueError, IndexError):
@@ -116,14 +134,23 @@ def ncu_traffic(kernel):
         return None
 
 
+def ref_route(sample, threads):
+    out = subprocess.run([REF_BENCH, "route", str(N_AGENTS), str(N_TIERS), str(sample), "oracle",
+                          str(threads), str(SEED)], capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def ref_sched(rounds):
+    out = subprocess.run([REF_BENCH, "sched", str(SCHED_INFLIGHT), str(SCHED_BEAM), str(rounds),
+                          str(SEED), "0"], capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
 def cpu_baseline(sample=CPU_SAMPLE_REQUESTS, threads=None):
     """The reference's own enumerate-mode loop on the host cores (ref_bench)."""
     threads = threads or os.cpu_count()
     if os.path.exists(REF_BENCH):
-        out = subprocess.run([REF_BENCH, "route", str(N_AGENTS), str(N_TIERS), str(sample),
-                              "oracle", str(threads), str(SEED)], capture_output=True, text=True,
-                             check=True).stdout
-        r = json.loads(out.strip().splitlines()[-1])
+        r = ref_route(sample, threads)
         return {"value": r["configs_per_s"], "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"first {sample} requests of config 2 "
                           f"({sample * N_TIERS ** N_AGENTS:.3g} configs), reference "
@@ -151,27 +178,106 @@ def run_reference(args):
     if not os.path.exists(REF_BENCH):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
         return
-    times, vals = [], []
+    vals = []
     for i in range(args.warmup + args.steps):
-        base = cpu_baseline(CPU_SAMPLE_REQUESTS, threads)
+        r = ref_route(CPU_SAMPLE_REQUESTS, threads)
         if i >= args.warmup:
-            vals.append(base["value"])
+            vals.append(r["configs_per_s"])
     v = statistics.median(vals)
     ms = CPU_SAMPLE_REQUESTS * N_TIERS ** N_AGENTS / v * 1e3
+    sched = ref_sched(args.sched_rounds + args.sched_warmup)
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "impl": "reference", "config": workload_config(1),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{CPU_SAMPLE_REQUESTS} requests of config 2 per step"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "sched": {"p50_us": sched["p50_us"], "p99_us": sched["p99_us"],
+                      "mean_us": sched["mean_us"], "rounds": sched["rounds"], "cores": 1,
+                      "decision_hash": sched["hash"],
+                      "what": "beam_schedule per round, reference C++ on one core"}}
     print(json.dumps(line))
+
+
+def run_sched(P, W, dev, args):
+    """Config 3 on this GPU: p50/p99 of the C-ABI round latency."""
+    c3 = W.Config3(dev, inflight=SCHED_INFLIGHT, rounds=args.sched_rounds + args.sched_warmup,
+                   seed=SEED, beam=SCHED_BEAM)
+    dev_us, capi_us = [], []
+
+    def on_round(rd, a):
+        if rd >= args.sched_warmup:
+            t = c3.sess.round_timing()
+            dev_us.append(float(t.sum()))
+            capi_us.append(c3.sess.last_round_us())
+
+    _, h, assigned = c3.run(on_round=on_round)
+    capi = np.asarray(capi_us)
+    devt = np.asarray(dev_us)
+    return {"p50_us": float(np.percentile(capi, 50)), "p99_us": float(np.percentile(capi, 99)),
+            "mean_us": float(capi.mean()),
+            "device_p50_us": float(np.percentile(devt, 50)),
+            "device_p99_us": float(np.percentile(devt, 99)),
+            "rounds": len(capi), "warmup_rounds": args.sched_warmup, "assigned": int(assigned),
+            "decision_hash": f"{h:016x}",
+            "what": "ag_sched_round wall time inside the C ABI (update upload + round kernel + "
+                    "assignment download); device = the round kernel alone"}
+
+
+def run_deep(P, args, ws, rank, local, barrier):
+    """Config 4: 8 stages x 12 tiers (4.3e8 configurations per request), 16
+    requests, the canonical-index space split contiguously across the ranks
+    (strong scaling), then one all-gather of per-shard records (counts and
+    the runtime-cost minimum) -- paper_2511_20975_b200.parallel."""
+    import torch
+
+    from paper_2511_20975_b200 import parallel as PL
+
+    n, m, R = 8, 12, 16
+    dev_t = torch.device("cuda", local)
+    space = P.ConfigSpace.chain(n, m)
+    dev = P.Device(space, local, torch.cuda.current_stream(dev_t))
+    batch = P.AccuracyBatch.generate(space, P.GenParams(), R, SEED)
+    truth = batch.to_device(dev_t)
+    router = P.OracleRouter()
+    begin, end = PL.shard_range(space.size, rank, ws)
+    probe = dev.route_enumerate(truth, router, begin, end, compact=False)
+    torch.cuda.synchronize()
+    cap = int(probe.offsets[-1])
+    out = dev.alloc_route(R, begin, end, cap)
+    mean = [0.05 + float(np.exp(-0.3 + 0.35 * i + 0.5 * 0.25 * 0.25)) for i in range(m)]
+    load = P.RuntimeCostContext([4] * m, [i % 3 for i in range(m)], [8] * m, mean)
+    times = []
+    steps = max(2, min(args.steps, 5))
+    for i in range(1 + steps):
+        barrier()
+        t0 = time.perf_counter()
+        res, total, before, best = PL.route_space_sharded(dev, truth, router, rank, ws, load, out=out)
+        barrier()
+        if i:
+            times.append(time.perf_counter() - t0)
+    dt = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev_t)
+    if ws > 1:
+        torch.distributed.all_reduce(dt, op=torch.distributed.ReduceOp.MAX)
+    dt = float(dt.item())
+    configs = R * space.size
+    del out, res, probe
+    torch.cuda.empty_cache()
+    return {"workload": "config4: chain 8 x 12 tiers (4.3e8 configs/request), 16 requests, "
+                        f"canonical-index space sharded over {ws} GPU(s), oracle router, "
+                        "enumerate + compact + runtime-cost argmin + all-gather of 32-byte "
+                        "per-shard records",
+            "configs_per_s": configs / dt, "ms_per_step": dt * 1e3, "scaling": "strong",
+            "members": int(total.sum()), "n_gpus": ws,
+            "timing": "host wall clock per sharded step, max over ranks, median of steps"}
 
 
 def run_ours(args):
     import torch
 
     import paper_2511_20975_b200 as P
+    from paper_2511_20975_b200 import workloads as W
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -180,6 +286,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev_t = torch.device("cuda", local)
+    clocks = Clocks(local)
 
     space = P.ConfigSpace.chain(N_AGENTS, N_TIERS)
     batch = P.AccuracyBatch.generate(space, P.GenParams(), REQUESTS_PER_GPU, SEED,
@@ -211,7 +318,6 @@ def run_ours(args):
     # ---- device-resident timed region (value) + live per-kernel profile
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
-    clocks = Clocks(local)
     launches0 = dev.launch_count
     barrier()
     dev.profile_begin()
@@ -222,7 +328,6 @@ def run_ours(args):
         ev[i][1].record(stream)
     kprof = dev.profile_end()
     barrier()
-    clk = clocks.stop()
     launches = dev.launch_count - launches0
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev_t)
@@ -231,6 +336,8 @@ def run_ours(args):
     tot_ms = float(tot_ms.item())
     configs_total = args.steps * REQUESTS_PER_GPU * S * ws
     value = configs_total / (tot_ms / 1e3)
+    # parity spot check of this run's output against its own bitmap count
+    ok_counts = int(out["offsets"][-1]) == total_members
 
     # ---- e2e through the host-buffer C ABI call (H2D + D2H inside the region)
     hb_counts = np.zeros(REQUESTS_PER_GPU, np.uint64)
@@ -254,8 +361,12 @@ def run_ours(args):
     h2d = (batch.request_ids.nbytes + batch.seed_ptr.nbytes + batch.seeds.nbytes +
            batch.removed_ptr.nbytes + batch.removed.nbytes)
     d2h = hb_counts.nbytes + hb_offsets.nbytes + 4 * total_members
-    ok = int(hb_offsets[-1]) == total_members
+    e2e_ok = int(hb_offsets[-1]) == total_members
     P.lib().ag_host_free(pinned)
+
+    sched = run_sched(P, W, dev, args) if rank == 0 and not args.no_sched else None
+    deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)
+    clk = clocks.stop()
 
     if rank != 0:
         if ws > 1:
@@ -264,11 +375,11 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (algorithmic bytes / avg duration)
     hbm, peak_src = peaks()
-    W = (S + 31) // 32
-    bitmap_bytes = REQUESTS_PER_GPU * W * 4
-    algo = {"k_route_score": bitmap_bytes,                       # bitmap write
-            "k_route_compact": bitmap_bytes + 4 * total_members,  # bitmap read + index write
-            "k_chunk_scan": REQUESTS_PER_GPU * (W // 32) * 12 + 8 * REQUESTS_PER_GPU,
+    W_words = (S + 31) // 32
+    bitmap_bytes = REQUESTS_PER_GPU * W_words * 4
+    algo = {"k_route_score": bitmap_bytes,                        # bitmap write
+            "k_route_compact": bitmap_bytes + 4 * total_members,   # bitmap read + index write
+            "k_chunk_scan": REQUESTS_PER_GPU * 16,
             "k_request_scan": 16 * REQUESTS_PER_GPU}
     dom = max(kprof, key=lambda k: kprof[k][0])
     dom_ms = kprof[dom][0] / kprof[dom][1]
@@ -281,7 +392,7 @@ def run_ours(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "impl": "ours", "config": workload_config(ws),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h), "members_ok": ok,
+                "d2h_bytes_per_step": int(d2h), "members_ok": bool(e2e_ok and ok_counts),
                 "path": "ag_route_enumerate_host (pinned host indices)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
@@ -289,10 +400,13 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": algo.get(dom, 0),
                      "avg_launch_ms": dom_ms},
         "path_roofline": {"bytes_per_step": path_bytes,
-                          "achieved_gbs": path_bytes / (tot_ms / args.steps / 1e3) / 1e9},
+                          "achieved_gbs": path_bytes / (tot_ms / args.steps / 1e3) / 1e9,
+                          "frac": path_bytes / (tot_ms / args.steps / 1e3) / 1e9 / hbm},
         "kernel_share": kernel_share,
         "members_per_step": total_members,
         "gpu_launches": int(launches),
+        "sched": sched,
+        "deep": deep,
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
@@ -308,7 +422,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--sched-rounds", type=int, default=150)
+    ap.add_argument("--sched-warmup", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sched", action="store_true")
+    ap.add_argument("--no-deep", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -25,8 +25,10 @@ int Scratch::ensure(size_t want) {
   if (want <= bytes) return AG_OK;
   if (p) cudaFree(p);
   p = nullptr;
+  // geometric growth: per-round buffers must not reallocate round after round
+  // (cudaFree synchronises the device)
+  size_t b = std::max<size_t>(std::max<size_t>(want, 256), bytes + bytes / 2);
   bytes = 0;
-  size_t b = std::max<size_t>(want, 256);
   cudaError_t e = cudaMalloc(&p, b);
   if (e != cudaSuccess) {
     p = nullptr;

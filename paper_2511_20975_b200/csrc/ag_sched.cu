@@ -1119,11 +1119,12 @@ namespace {
 
 int ensure_pinned(void** p, size_t* have, size_t bytes) {
   if (bytes <= *have) return AG_OK;
+  const size_t b = std::max<size_t>(std::max<size_t>(bytes, 4096), *have + *have / 2);
   if (*p) cudaFreeHost(*p);
   *p = nullptr;
   *have = 0;
-  AG_CUDA(cudaMallocHost(p, std::max<size_t>(bytes, 4096)));
-  *have = std::max<size_t>(bytes, 4096);
+  AG_CUDA(cudaMallocHost(p, b));
+  *have = b;
   return AG_OK;
 }
 

@@ -147,4 +147,7 @@ class Config3:
                 for s in done:
                     del self.stages[s]
                 self._fill()
+            # the dispatch / arrival kernels finish outside the next round's
+            # timed decision
+            self.dev.synchronize()
         return np.asarray(lat), h, assigned
