@@ -278,9 +278,12 @@ int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width,
 /* Request::mark_dispatched for applied triples (request.cpp:70-86): prefix
  * prune of the viable list in HBM, stage -> in flight. */
 int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied);
-/* diagnostics: device timestamps (ns) of the last round's phases:
- * start, context built, candidates compacted, walk done, finalized */
-int ag_sched_round_timing(ag_sched* s, uint64_t* ns5);
+/* diagnostics of the last round, 16 u64: [0..4] device timestamps (ns):
+ * start, deltas applied, first candidates published, walk done, finalized;
+ * [5..8] walk cycles (find, build, rank, adopt); [9..10] walk steps and
+ * children; [11..14] timestamps of the first producer chunk (loads, scan,
+ * records, histogram rows) */
+int ag_sched_round_timing(ag_sched* s, uint64_t* out16);
 /* host wall time (us) of the last ag_sched_round call, entry to return */
 double ag_sched_last_round_us(const ag_sched* s);
 /* read back one request's current viable list (host buffer) */

@@ -15,25 +15,36 @@
 // so a round never rescans viable lists except on the rare re-touch of a
 // request with parallel ready branches.
 //
-// One round = one CTA (k_sched_round):
-//   A. block-parallel RoundContext over the FIFO queue (loads batched per
-//      thread so the dependent order -> ready -> cand chain costs a few memory
-//      latencies, not one per request): pairs in (arrival, id) x (depth desc,
-//      declaration asc) order, validation, and the compacted list of
-//      "candidate" pairs -- those whose candidate models meet the engines free
-//      at round start.  Every other pair is a whole-beam skip in every branch
-//      (scheduler.cpp:317-329), so the walk never looks at it.  Candidates get
-//      (position, mask) in shared memory and, for the first few thousand,
-//      their request details and model histogram row too.
-//   B. warp 0 walks the candidates exactly as beam_schedule walks pairs:
-//      skipped runs are fast-forwarded with one ballot scan; at a step lanes
-//      are children (extend_state); nested retention (scheduler.cpp:351-370)
-//      is a warp bitonic sort under the exact state_better order followed by
-//      one ballot per beam level; a child's triple list is a node of a history
-//      tree (triples_less compares two tree paths).
-//   C. finalize: the winner's triples from the tree (written in parallel),
-//      score_assignment's utilization and flexibility folded in the
-//      reference's order.
+// One round = one launch of k_sched_round (one CTA of 512 threads):
+//   * producer warps (every warp not on the walker's SM sub-partition: wid %
+//     4 != 0) scan the FIFO queue chunk by chunk -- RoundContext
+//     (scheduler.cpp:36-72): pairs in (arrival, id) x (depth desc,
+//     declaration asc) order, validation, and the compacted list of
+//     "candidate" pairs, those whose candidate models meet the engines free
+//     at round start.  Every other pair is a whole-beam skip in every branch
+//     (scheduler.cpp:317-329), so the walk never looks at it.  Candidates
+//     (pair position, engine mask, request details and, for the head of the
+//     list, the model histogram row with the first-touch flexibility ratios
+//     surv / initial already divided) are published through a
+//     release/acquire counter in shared memory;
+//   * warp 0 walks the candidates as beam_schedule walks pairs, starting as
+//     soon as the first chunk is published: skipped runs are fast-forwarded
+//     with one ballot scan; beam state w lives in the registers of lane w; at
+//     a step lane c builds child c (extend_state), ranks it against the other
+//     children under the exact state_better order, and nested retention
+//     (scheduler.cpp:351-370) is B warp min-reductions over those ranks; a
+//     child's triple list is a node of a history tree (triples_less compares
+//     two tree paths through a per-step LCP structure).  The walk stops as
+//     soon as every branch is full or the candidates are exhausted; the
+//     queue's pair count comes from the host mirror, so the producers stop
+//     scanning once the walker is done (unless validation needs every pair);
+//   * finalize: the winner's triples from the tree (written in parallel),
+//     score_assignment's utilization and flexibility folded in the
+//     reference's order;
+//   * the round's input deltas (ready masks, FIFO tail) are read by the
+//     kernel from mapped pinned host memory and the assignment is written
+//     straight back into it: one launch and one stream synchronisation per
+//     round, no separate copies.
 // All fp64 arithmetic repeats the reference's operations in the same order
 // (the library builds with --fmad=false).
 #include <cuda_runtime.h>
@@ -51,11 +62,13 @@ namespace agb {
 
 namespace {
 
-constexpr int kRoundThreads = 512;  // 128 registers per thread: no local memory in the walk
+constexpr int kRoundThreads = 512;
+constexpr int kProducers = 384;  // warps 1-3, 5-7, 9-11, 13-15
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
 constexpr int kSmemNodes = 1024;
-constexpr int kPer = 8;  // FIFO positions per thread per pass chunk
+constexpr int kPer = 4;  // FIFO positions per producer thread per chunk
+constexpr unsigned kFull = 0xffffffffu;
 
 struct Node {  // one AssignmentTriple in the beam history tree
   int32_t qi;
@@ -68,28 +81,11 @@ struct Node {  // one AssignmentTriple in the beam history tree
   int32_t pad;
 };
 
-struct Det {  // details of one candidate pair
-  int32_t qi;
-  int32_t slot;
-  uint32_t nvia;
-  int32_t agent;
-};
-
-struct BState {  // BeamState (scheduler.cpp:80-93)
-  double util, flex_sum;
-  long long skips;
-  int flex_count;
-  uint32_t free_mask;
-  int node;  // latest history node, -1 = no triple
-  int nsurv; // survivors of the request of `node`
-  int occ[kMaxEng];
-};
-
-struct Child {
-  double util, flex_sum, flex;
-  long long skips;
-  int flex_count, nsurv;
-  int16_t parent, eng;  // eng < 0: skip child
+struct Cand {  // one candidate pair
+  uint32_t pos;         // pair position in the round's two-level order
+  int32_t qi;           // request index (queue container order)
+  uint32_t slot_agent;  // slot | agent << 26
+  uint32_t nvia;        // round-start viable size
 };
 
 struct EngDev {
@@ -104,19 +100,25 @@ struct EngDev {
 
 struct RoundArgs {
   int N, M, B;
-  const int32_t* order;  // [Q] slots in FIFO order (dead slots have ready 0)
-  const int32_t* cidx;   // [Q] container index per FIFO position, or null
-  int Q;
+  int Q;                 // FIFO length (dead slots have ready 0)
+  long long npairs;      // ready pairs in the queue (host mirror)
+  int32_t* order;        // [Q] slots in FIFO order (device)
+  int32_t* cidx;         // [Q] container index per FIFO position (device), or null
   uint64_t* ready;
-  int n_upd;
-  const int32_t* upd_slot;
-  const uint64_t* upd_mask;
   const uint32_t* cand;
   const uint32_t* hist;
-  const uint32_t* nviable;
   const uint64_t* voff;
   const uint32_t* pool;
+  const uint32_t* nviable;
   const uint64_t* ids;
+  const uint32_t* ever;  // OR of every candidate-model mask ever installed
+  // round input deltas in mapped pinned host memory
+  const uint64_t* h_upd_mask;
+  const int32_t* h_upd_slot;
+  int n_upd;
+  const int32_t* h_tail;  // FIFO tail, lands at order[tail_from ..]
+  int tail_from, n_tail;
+  const int32_t* h_cidx;  // [Q] or null
   int8_t prio[64];
   int8_t prio_rank[64];
   uint32_t place[kMaxAgents];
@@ -124,17 +126,17 @@ struct RoundArgs {
   uint64_t div_m;
   EngDev eng;
   // scratch
-  uint32_t* gcpos;  // candidate positions / masks beyond shared memory
-  uint32_t* gcmask;
-  Det* gdet;  // candidate details beyond shared memory
-  int cand_cap, det_cap, hist_cap;
+  uint32_t* gmask;  // candidates beyond shared memory
+  Cand* grec;
+  int cand_cap, hist_cap;
   Node* gnodes;
   int max_nodes;
   int max_children;
-  // outputs: one contiguous block copied back in a single transfer
-  int32_t* out;  // [0] status [1] queue size | ag_assignment | occ[32] | triples
+  // outputs (mapped pinned host memory): [0] status [1] aux | ag_assignment |
+  // occ[32] | triples
+  int32_t* out;
   int triples_cap;
-  unsigned long long* timing;  // [5] globaltimer at phase boundaries (ns)
+  unsigned long long* timing;  // [13]: globaltimer marks, walk/scan cycle buckets
   int32_t* async_status;       // errors latched by earlier dispatch / add kernels
 };
 
@@ -145,6 +147,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.cta.shared.u32 %0, [%1];"
+               : "=r"(v)
+               : "r"((unsigned)__cvta_generic_to_shared(p))
+               : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+               : "memory");
+}
+
+__device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory"); }
 
 __device__ __forceinline__ uint32_t digit_at(uint32_t c, int a, const RoundArgs& A) {
   const uint32_t q = A.place[a] == 1 ? c : (uint32_t)__umul64hi(c, A.place_magic[a]);
@@ -160,88 +178,127 @@ struct NodeView {
   }
 };
 
-__device__ __forceinline__ int depth_of(const NodeView& nv, int n) {
-  return n < 0 ? 0 : nv[n].depth;
-}
-
-// Per-step lexicographic structure of the beam states' triple lists, so that
-// triples_less (scheduler.cpp:95-105) costs O(1): lcp[i][j] is the length of
-// the common prefix of states i and j, nxt[i][j] the key of state i's element
-// at that position (kEnd when its list ends there).  Adopting children updates
-// it in O(B^2): two children of one parent share its whole list; children of
-// different parents keep their parents' common prefix.
-constexpr uint64_t kEnd = 0;  // below every triple key
+// triples_less (scheduler.cpp:95-105) between the beam states' triple lists,
+// kept as a relation per ordered pair of states instead of the lists: rel[i][j]
+// is LESS / GREATER when the lists differ at a position both have, P1 when
+// list i is a proper prefix of list j (then the low bits hold list j's element
+// at that position), P2 when list j is a proper prefix of list i (low bits:
+// list i's element there).  A triple key orders (request_index, agent, model)
+// lexicographically; kEnd sorts below every key.  Every pair (request, agent)
+// is visited once per walk, so a step's key never equals an element of an
+// earlier list, and distinct states never hold equal lists.  Adopting children
+// updates the relation in O(B^2) without touching the lists.
+constexpr uint64_t kEnd = 0;
+constexpr uint64_t kRelLess = 0, kRelGreater = 1ull << 62, kRelP1 = 2ull << 62, kRelP2 = 3ull << 62;
+constexpr uint64_t kRelCode = 3ull << 62, kRelThr = ~kRelCode;
 
 __device__ __forceinline__ uint64_t tkey(int qi, int agent, int model) {
   return ((uint64_t)(uint32_t)(qi + 1) << 32) | ((uint64_t)(uint32_t)agent << 16) |
          (uint64_t)(uint32_t)model;
 }
 
-struct Lex {
-  int len[kMaxBeam];
-  int lcp[kMaxBeam][kMaxBeam];
-  uint64_t nxt[kMaxBeam][kMaxBeam];
-};
-
-// triples_less between item (parent p1 + extra k1) and (p2 + k2); k = kEnd
-// for "no extra".  Items with p1 == p2 differ only in their extras.
-__device__ __forceinline__ bool lex_less(const Lex& L, int p1, uint64_t k1, int p2, uint64_t k2) {
-  if (p1 == p2) return k1 < k2;
-  const int l = L.lcp[p1][p2];
-  const uint64_t y1 = l < L.len[p1] ? L.nxt[p1][p2] : k1;
-  const uint64_t y2 = l < L.len[p2] ? L.nxt[p2][p1] : k2;
-  return y1 < y2;
+// relation of (list p1 + k1) to (list p2 + k2); k = kEnd for "no extra";
+// r12 = rel[p1][p2] (unused when p1 == p2)
+__device__ __forceinline__ uint64_t rel_extend(bool same, uint64_t r12, uint64_t k1, uint64_t k2) {
+  if (same) {  // one parent: its children differ in the extra key
+    if (k1 == kEnd) return kRelP1 | k2;
+    if (k2 == kEnd) return kRelP2 | k1;
+    return k1 < k2 ? kRelLess : kRelGreater;
+  }
+  const uint64_t code = r12 & kRelCode, thr = r12 & kRelThr;
+  if (code == kRelP1) return k1 == kEnd ? r12 : (k1 < thr ? kRelLess : kRelGreater);
+  if (code == kRelP2) return k2 == kEnd ? r12 : (thr < k2 ? kRelLess : kRelGreater);
+  return r12;
 }
 
-struct WalkCtx {
-  const Child* ch;
-  const Lex* L;
-  uint64_t key_base;  // tkey(qcur, agent, 0)
-  const EngDev* eng;
-  __device__ __forceinline__ uint64_t key(int c) const {
-    return ch[c].eng >= 0 ? key_base | (uint64_t)(uint32_t)eng->model[ch[c].eng] : kEnd;
-  }
-  // strict total order: state_better (scheduler.cpp:109-115), then the lower
-  // child index (retention adopts the first best child, scheduler.cpp:357-362)
-  __device__ __forceinline__ bool before(int c1, int c2) const {
-    if (c1 < 0) return false;
-    if (c2 < 0) return true;
-    const Child &x = ch[c1], &y = ch[c2];
-    if (x.util != y.util) return x.util > y.util;
-    if (x.flex != y.flex) return x.flex > y.flex;
-    if (x.skips != y.skips) return x.skips < y.skips;
-    const uint64_t k1 = key(c1), k2 = key(c2);
-    if (lex_less(*L, x.parent, k1, y.parent, k2)) return true;
-    if (lex_less(*L, y.parent, k2, x.parent, k1)) return false;
-    return c1 < c2;
-  }
+// list 1 before list 2 (triples_less); lists of distinct items never compare equal
+__device__ __forceinline__ bool rel_before(uint64_t r) {
+  const uint64_t code = r & kRelCode;
+  return code == kRelLess || code == kRelP1;
+}
+
+// (list p1 + k1) strictly before (list p2 + k2), branch-free: the common
+// case of rel_before(rel_extend(...)).  kEnd = 0 sorts below every threshold.
+__device__ __forceinline__ bool lex_before(bool same, uint64_t r12, uint64_t k1, uint64_t k2) {
+  const uint64_t code = r12 & kRelCode, thr = r12 & kRelThr;
+  const bool by_rel = (code == kRelLess) | ((code == kRelP1) & (k1 < thr)) | ((code == kRelP2) & (thr < k2));
+  return same ? (k1 < k2) : by_rel;
+}
+
+// rel_extend without branches
+__device__ __forceinline__ uint64_t rel_extend_sel(bool same, uint64_t r12, uint64_t k1, uint64_t k2) {
+  const uint64_t code = r12 & kRelCode, thr = r12 & kRelThr;
+  const uint64_t lg = k1 < k2 ? kRelLess : kRelGreater;
+  const uint64_t s_res = k1 == kEnd ? (kRelP1 | k2) : (k2 == kEnd ? (kRelP2 | k1) : lg);
+  const uint64_t p1 = k1 == kEnd ? r12 : (k1 < thr ? kRelLess : kRelGreater);
+  const uint64_t p2 = k2 == kEnd ? r12 : (thr < k2 ? kRelLess : kRelGreater);
+  const uint64_t o_res = code == kRelP1 ? p1 : (code == kRelP2 ? p2 : r12);
+  return same ? s_res : o_res;
+}
+
+// order-preserving u64 image of an f64 (no NaNs here; -0 == +0)
+__device__ __forceinline__ uint64_t okey(double d) {
+  uint64_t b = (uint64_t)__double_as_longlong(d);
+  if (b == 0x8000000000000000ull) b = 0;
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// rank record of a child: state_better keys (scheduler.cpp:109-115)
+struct RankKey {
+  uint64_t ku, kf;  // okey(util), okey(flexibility): larger is better
+  uint32_t sk;      // skips: fewer is better
+  uint32_t pk;      // parent | (model + 1) << 8, 0 for the skip child
+  uint64_t pad;
+};
+
+struct Child {  // a BeamState child in shared memory (wide beams)
+  double util, flex_sum, flex;
+  long long skips;
+  int flex_count, nsurv;
+  int16_t parent, eng;  // eng < 0: skip child
+  int pad;
 };
 
 // ------------------------------------------------------------ round kernel
 __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ BState st[2][kMaxBeam];
-  __shared__ Lex lex[2];
+  __shared__ int s_occ[2][kMaxBeam][kMaxEng];
+  __shared__ uint64_t s_rel[2][kMaxBeam][kMaxBeam];
+  __shared__ __align__(16) RankKey s_rk[32];
   __shared__ int s_cnt[kMaxBeam][32];
-  __shared__ long long s_scan[kRoundThreads / 32][3];
-  __shared__ long long s_carry[3];
-  __shared__ int s_status;
   __shared__ int s_picked[kMaxBeam];
   __shared__ int s_cons[kMaxAgents][2];
   __shared__ int s_ncons;
-  // dynamic: nodes | children | cand pos | cand mask | details | hist rows
+  __shared__ long long s_scan[kProducers / 32][3];
+  __shared__ long long s_carry[3];
+  __shared__ int s_chunk[2];     // candidates of the current chunk: [first, end)
+  __shared__ int s_status;       // producer-detected validation error
+  __shared__ int s_stop;         // producers: snapshot of s_walk_done
+  __shared__ unsigned s_produced;  // candidates published (release/acquire)
+  __shared__ unsigned s_rows;      // candidates whose histogram rows are staged
+  __shared__ unsigned s_prod_done;
+  __shared__ unsigned s_walk_done;
+  __shared__ int e_model[kMaxEng], e_slots[kMaxEng];
+  __shared__ double e_weight[kMaxEng];
+  __shared__ int8_t e_m2e[32], s_prio[64], s_prank[64];
+  __shared__ uint32_t s_emtab[4][256];  // model mask -> engine mask, one byte at a time
+  // dynamic: nodes | children (wide beams) | ratio rows | cand records | cand masks | count rows
   Node* s_nodes = reinterpret_cast<Node*>(dsm);
   Child* children = reinterpret_cast<Child*>(s_nodes + kSmemNodes);
-  uint32_t* c_pos = reinterpret_cast<uint32_t*>(children + A.max_children);
-  uint32_t* c_mask = c_pos + A.cand_cap;
-  Det* c_det = reinterpret_cast<Det*>(c_mask + A.cand_cap);
-  uint32_t* c_hist = reinterpret_cast<uint32_t*>(c_det + A.det_cap);
+  double* h_rat = reinterpret_cast<double*>(children + A.max_children);
+  Cand* c_rec = reinterpret_cast<Cand*>(h_rat + (size_t)A.hist_cap * A.M);
+  uint32_t* c_mask = reinterpret_cast<uint32_t*>(c_rec + A.cand_cap);
+  uint32_t* h_cnt = c_mask + A.cand_cap;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int T = blockDim.x;
   const int N = A.N, M = A.M, B = A.B;
   if (tid == 0) {
     s_status = 0;
+    s_stop = 0;
+    s_produced = 0;
+    s_rows = 0;
+    s_prod_done = 0;
+    s_walk_done = 0;
     s_carry[0] = s_carry[1] = s_carry[2] = 0;
     if (A.timing) A.timing[0] = gtimer();
     if (*A.async_status) {
@@ -249,241 +306,372 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       *A.async_status = 0;
     }
   }
-  for (int i = tid; i < A.n_upd; i += T) A.ready[A.upd_slot[i]] = A.upd_mask[i];
+  if (tid < kMaxEng) {
+    e_model[tid] = A.eng.model[tid];
+    e_slots[tid] = A.eng.slots[tid];
+    e_weight[tid] = A.eng.weight[tid];
+    e_m2e[tid] = A.eng.m2e[tid];
+  }
+  if (tid < 64) {
+    s_prio[tid] = A.prio[tid];
+    s_prank[tid] = A.prio_rank[tid];
+  }
+  for (int i = tid; i < 1024; i += kRoundThreads) {
+    uint32_t em = 0;
+    for (int b = 0; b < 8; ++b) {
+      const int e = A.eng.m2e[(i >> 8) * 8 + b];
+      if (((i >> b) & 1) && e >= 0) em |= 1u << e;
+    }
+    s_emtab[i >> 8][i & 255] = em;
+  }
+  // the round's deltas (mapped host memory, small): FIFO tail, container
+  // indices, ready masks -- loads issued in batches so PCIe latency is paid
+  // once per batch
+  {
+    constexpr int kU = 4;
+    for (int i0 = 0; i0 < A.n_tail; i0 += kRoundThreads * kU) {
+      int32_t v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kRoundThreads + tid;
+        v[u] = i < A.n_tail ? A.h_tail[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kRoundThreads + tid;
+        if (i < A.n_tail) A.order[A.tail_from + i] = v[u];
+      }
+    }
+    if (A.h_cidx)
+      for (int i0 = 0; i0 < A.Q; i0 += kRoundThreads * kU) {
+        int32_t v[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + u * kRoundThreads + tid;
+          v[u] = i < A.Q ? A.h_cidx[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + u * kRoundThreads + tid;
+          if (i < A.Q) A.cidx[i] = v[u];
+        }
+      }
+    for (int i0 = 0; i0 < A.n_upd; i0 += kRoundThreads * kU) {
+      int32_t sl[kU];
+      uint64_t mk[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kRoundThreads + tid;
+        sl[u] = i < A.n_upd ? A.h_upd_slot[i] : -1;
+        mk[u] = i < A.n_upd ? A.h_upd_mask[i] : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (sl[u] >= 0) A.ready[sl[u]] = mk[u];
+    }
+  }
   __syncthreads();
   if (s_status) {
     if (tid == 0) A.out[0] = s_status;
     return;
   }
+  if (tid == 0 && A.timing) A.timing[1] = gtimer();
   // engines / models with a free slot at round start
   uint32_t U0 = 0, U0m = 0;
   for (int e = 0; e < A.eng.E; ++e)
-    if (A.eng.slots[e] - A.eng.occ[e] > 0) {
+    if (e_slots[e] - A.eng.occ[e] > 0) {
       U0 |= 1u << e;
-      if (A.eng.model[e] < 32) U0m |= 1u << A.eng.model[e];
+      if (e_model[e] < 32) U0m |= 1u << e_model[e];
     }
+  // every pair must be scanned for RoundContext validation only if some
+  // installed candidate model has no pool
+  const bool check_all = (*A.ever & ~A.eng.mapped) != 0u;
 
-  // ---- A: RoundContext (scheduler.cpp:36-72) in chunks of T*kPer positions.
-  // Loads are batched per thread (slot -> ready -> cand/nviable) so the
-  // dependent chain costs three memory latencies per chunk.
-  long long ta[4] = {0, 0, 0, 0};
-  long long tq = clock64();
-  for (int base = 0; base < A.Q; base += T * kPer) {
-    const int p0 = base + tid * kPer;
-    int slot[kPer];
-    uint64_t rdy[kPer];
-    uint32_t cm1[kPer], nvia[kPer];
-    int a1[kPer];
+  if (wid != 0) {
+    if ((wid & 3) == 0) return;  // the walker's SM sub-partition stays quiet
+    // ================================================= producers
+    const int pt = tid - 32 * (1 + (wid >> 2));  // 0 .. kProducers-1
+    const int pw = pt >> 5;
+    for (int base = 0; base < A.Q; base += kProducers * kPer) {
+      if (s_stop) break;  // uniform: written before the previous barrier
+      const int p0 = base + pt * kPer;
+      int slot[kPer], a1[kPer];
+      uint64_t rdy[kPer];
+      uint32_t cm1[kPer], nvia[kPer];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) slot[i] = p0 + i < A.Q ? __ldg(A.order + p0 + i) : -1;
+      for (int i = 0; i < kPer; ++i) slot[i] = p0 + i < A.Q ? A.order[p0 + i] : -1;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) rdy[i] = slot[i] >= 0 ? A.ready[slot[i]] : 0ull;
+      for (int i = 0; i < kPer; ++i) rdy[i] = slot[i] >= 0 ? A.ready[slot[i]] : 0ull;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      // first ready agent in (depth desc, declaration asc) order
-      int best = -1, br = 1 << 30;
-      for (uint64_t b = rdy[i]; b; b &= b - 1) {
-        const int a = __ffsll((long long)b) - 1;
-        if (A.prio_rank[a] < br) br = A.prio_rank[a], best = a;
-      }
-      a1[i] = best;
-      cm1[i] = best >= 0 ? A.cand[(size_t)slot[i] * N + best] : 0u;
-      nvia[i] = best >= 0 ? A.nviable[slot[i]] : 0u;
-    }
-    { const long long t = clock64(); ta[0] += t - tq; tq = t; }
-    // pass 1: counts (pairs, requests, candidates) of this thread's positions
-    long long np = 0, nq = 0, nc = 0;
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      if (!rdy[i]) continue;
-      np += __popcll(rdy[i]);
-      nq += 1;
-      if ((rdy[i] & (rdy[i] - 1)) == 0) {  // one ready agent (chains): no more loads
-        bad |= (cm1[i] & ~A.eng.mapped) != 0;
-        nc += (cm1[i] & U0m) != 0;
-      } else {
+      for (int i = 0; i < kPer; ++i) {
+        // first ready agent in (depth desc, declaration asc) order
+        int best = -1, br = 1 << 30;
         for (uint64_t b = rdy[i]; b; b &= b - 1) {
           const int a = __ffsll((long long)b) - 1;
-          const uint32_t cm = A.cand[(size_t)slot[i] * N + a];
-          bad |= (cm & ~A.eng.mapped) != 0;
-          nc += (cm & U0m) != 0;
+          if (s_prank[a] < br) br = s_prank[a], best = a;
+        }
+        a1[i] = best;
+        cm1[i] = best >= 0 ? A.cand[(size_t)slot[i] * N + best] : 0u;
+        nvia[i] = best >= 0 ? A.nviable[slot[i]] : 0u;
+      }
+      // pass 1: counts (pairs, requests, candidates) of this thread's positions
+      long long np = 0, nq = 0, nc = 0;
+      bool bad = false;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        if (!rdy[i]) continue;
+        np += __popcll(rdy[i]);
+        nq += 1;
+        if ((rdy[i] & (rdy[i] - 1)) == 0) {  // one ready agent (chains): no more loads
+          bad |= (cm1[i] & ~A.eng.mapped) != 0;
+          nc += (cm1[i] & U0m) != 0;
+        } else {
+          for (uint64_t b = rdy[i]; b; b &= b - 1) {
+            const int a = __ffsll((long long)b) - 1;
+            const uint32_t cm = A.cand[(size_t)slot[i] * N + a];
+            bad |= (cm & ~A.eng.mapped) != 0;
+            nc += (cm & U0m) != 0;
+          }
         }
       }
-    }
-    if (bad) s_status = AG_ERR_VALIDATION + 100;  // viable tier without a pool
-    { const long long t = clock64(); ta[1] += t - tq; tq = t; }
-    long long x[3] = {np, nq, nc};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1)
-#pragma unroll
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const long long y = __shfl_up_sync(0xffffffffu, x[k], o);
-        if (lane >= o) x[k] += y;
-      }
-    if (lane == 31)
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) s_scan[wid][k] = x[k];
-    __syncthreads();
-    if (wid == 0) {
-      long long v[3], z[3];
-      #pragma unroll
-      for (int k = 0; k < 3; ++k) v[k] = z[k] = lane < T / 32 ? s_scan[lane][k] : 0;
+      if (bad) s_status = AG_ERR_VALIDATION + 100;  // viable tier without a pool
+      if (base == 0 && pt == 0 && A.timing) A.timing[11] = gtimer();
+      long long x[3] = {np, nq, nc};
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1)
-        #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const long long y = __shfl_up_sync(0xffffffffu, z[k], o);
-          if (lane >= o) z[k] += y;
-        }
-      if (lane < T / 32)
-        #pragma unroll
-        for (int k = 0; k < 3; ++k) s_scan[lane][k] = z[k] - v[k] + s_carry[k];
-      __syncwarp();
-      if (lane == 31)
-        #pragma unroll
-        for (int k = 0; k < 3; ++k) s_carry[k] += z[k];
-    }
-    __syncthreads();
-    { const long long t = clock64(); ta[2] += t - tq; tq = t; }
-    // pass 2: write this thread's candidates (position, engine mask, details,
-    // histogram row) in pair order
-    int pos = (int)(s_scan[wid][0] + x[0] - np);
-    int qr = (int)(s_scan[wid][1] + x[1] - nq);
-    int cw = (int)(s_scan[wid][2] + x[2] - nc);
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-      if (!rdy[i]) continue;
-      const int qi = A.cidx ? A.cidx[p0 + i] : qr;
-      ++qr;
-      const bool single = (rdy[i] & (rdy[i] - 1)) == 0;
-      for (int t = 0; t < N; ++t) {
-        const int a = single ? a1[i] : A.prio[t];
-        if (!single && !((rdy[i] >> a) & 1ull)) continue;
-        const uint32_t cm = single ? cm1[i] : A.cand[(size_t)slot[i] * N + a];
-        if (cm & U0m) {
-          uint32_t em = 0;  // engine mask of the candidate models
-          for (uint32_t b = cm; b; b &= b - 1) em |= 1u << A.eng.m2e[__ffs(b) - 1];
-          if (cw < A.cand_cap) {
-            c_pos[cw] = (uint32_t)pos;
-            c_mask[cw] = em & U0;
-          } else {
-            A.gcpos[cw - A.cand_cap] = (uint32_t)pos;
-            A.gcmask[cw - A.cand_cap] = em & U0;
-          }
-          const Det d{qi, slot[i], nvia[i], a};
-          if (cw < A.det_cap) c_det[cw] = d;
-          else A.gdet[cw - A.det_cap] = d;
-          if (cw < A.hist_cap) {
-            const uint32_t* hr = A.hist + ((size_t)slot[i] * N + a) * M;
-            for (int mdl = 0; mdl < M; ++mdl) c_hist[cw * M + mdl] = __ldg(hr + mdl);
-          }
-          ++cw;
+        for (int k = 0; k < 3; ++k) {
+          const long long y = __shfl_up_sync(kFull, x[k], o);
+          if (lane >= o) x[k] += y;
         }
-        ++pos;
-        if (single) break;
+      if (lane == 31)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) s_scan[pw][k] = x[k];
+      bar_producers();
+      if (pw == 0) {
+        constexpr int NW = kProducers / 32;
+        long long v[3], z[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = z[k] = lane < NW ? s_scan[lane][k] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const long long y = __shfl_up_sync(kFull, z[k], o);
+            if (lane >= o) z[k] += y;
+          }
+        if (lane < NW)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) s_scan[lane][k] = z[k] - v[k] + s_carry[k];
+        __syncwarp();
+        if (lane == 31) {
+          s_chunk[0] = (int)s_carry[2];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) s_carry[k] += z[k];
+          s_chunk[1] = (int)s_carry[2];
+        }
       }
+      bar_producers();
+      if (base == 0 && pt == 0 && A.timing) A.timing[12] = gtimer();
+      // pass 2: this thread's candidates (position, engine mask, details) in pair order
+      int pos = (int)(s_scan[pw][0] + x[0] - np);
+      int qr = (int)(s_scan[pw][1] + x[1] - nq);
+      int cw = (int)(s_scan[pw][2] + x[2] - nc);
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        if (!rdy[i]) continue;
+        const int qi = A.cidx ? A.cidx[p0 + i] : qr;
+        ++qr;
+        const bool single = (rdy[i] & (rdy[i] - 1)) == 0;
+        for (int t = 0; t < N; ++t) {
+          const int a = single ? a1[i] : s_prio[t];
+          if (!single && !((rdy[i] >> a) & 1ull)) continue;
+          const uint32_t cm = single ? cm1[i] : A.cand[(size_t)slot[i] * N + a];
+          if (cm & U0m) {
+            // engine mask of the candidate models
+            const uint32_t em = s_emtab[0][cm & 255] | s_emtab[1][(cm >> 8) & 255] |
+                                s_emtab[2][(cm >> 16) & 255] | s_emtab[3][cm >> 24];
+            const Cand r{(uint32_t)pos, qi, (uint32_t)slot[i] | ((uint32_t)a << 26), nvia[i]};
+            if (cw < A.cand_cap) {
+              c_mask[cw] = em & U0;
+              c_rec[cw] = r;
+            } else {
+              A.gmask[cw - A.cand_cap] = em & U0;
+              A.grec[cw - A.cand_cap] = r;
+            }
+            ++cw;
+          }
+          ++pos;
+          if (single) break;
+        }
+      }
+      bar_producers();
+      if (base == 0 && pt == 0 && A.timing) A.timing[13] = gtimer();
+      // pass 3: for the head of the list, the histogram rows with the
+      // first-touch flexibility ratios (extend_state, scheduler.cpp:182-191)
+      // -- one (candidate, model) entry per thread, loads in parallel.  The
+      // first rows of the chunk are published with its records, the rest
+      // right after.
+      const int c_lo = s_chunk[0], c_hi = min(s_chunk[1], A.hist_cap);
+      const int c_mid = min(c_hi, c_lo + 32);
+      auto stage_rows = [&](int from, int to) {
+        constexpr int kU = 4;
+        for (int e0 = from * M; e0 < to * M; e0 += kProducers * kU) {
+          uint32_t sv[kU], nvv[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int e = e0 + u * kProducers + pt;
+            sv[u] = 0;
+            nvv[u] = 1;
+            if (e < to * M) {
+              const int c = e / M, mdl = e - c * M;
+              const Cand r = c_rec[c];
+              const int a = (int)(r.slot_agent >> 26), sl = (int)(r.slot_agent & 0x3ffffffu);
+              sv[u] = __ldg(A.hist + ((size_t)sl * N + a) * M + mdl);
+              nvv[u] = r.nvia;
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int e = e0 + u * kProducers + pt;
+            if (e < to * M) {
+              h_cnt[e] = sv[u];
+              h_rat[e] = (double)sv[u] / (double)nvv[u];
+            }
+          }
+        }
+      };
+      stage_rows(c_lo, c_mid);
+      bar_producers();
+      if (pt == 0) {
+        if (base == 0 && A.timing) A.timing[14] = gtimer();
+        __threadfence_block();
+        if (c_mid > c_lo) st_release(&s_rows, (unsigned)c_mid);
+        st_release(&s_produced, (unsigned)s_carry[2]);
+      }
+      if (c_hi > c_mid) {
+        stage_rows(c_mid, c_hi);
+        bar_producers();
+        if (pt == 0) {
+          __threadfence_block();
+          st_release(&s_rows, (unsigned)c_hi);
+        }
+      }
+      if (pt == 0) s_stop = check_all ? 0 : (int)*(volatile unsigned*)&s_walk_done;
+      bar_producers();
     }
-    __syncthreads();
-    { const long long t = clock64(); ta[3] += t - tq; tq = t; }
-  }
-  if (tid == 0 && A.timing)
-    #pragma unroll
-    for (int k = 0; k < 4; ++k) A.timing[9 + k] = (unsigned long long)ta[k];
-  const int npairs = (int)s_carry[0], nreq = (int)s_carry[1], ncand = (int)s_carry[2];
-  if (tid == 0 && A.timing) A.timing[1] = gtimer();
-  if (s_status) {
-    if (tid == 0) A.out[0] = s_status;
+    if (pt == 0) {
+      __threadfence_block();
+      st_release(&s_prod_done, 1u);
+    }
     return;
   }
-  if (wid != 0) return;
-  if (lane == 0 && A.timing) A.timing[2] = gtimer();
 
-  // ---- B: the beam walk (warp 0)
+  // =================================================== walker (warp 0)
   const NodeView nv{s_nodes, A.gnodes};
   const int E = A.eng.E;
-  auto cposf = [&](int j) -> int { return (int)(j < A.cand_cap ? c_pos[j] : A.gcpos[j - A.cand_cap]); };
-  auto cmaskf = [&](int j) -> uint32_t { return j < A.cand_cap ? c_mask[j] : A.gcmask[j - A.cand_cap]; };
-  auto detf = [&](int j) -> Det { return j < A.det_cap ? c_det[j] : A.gdet[j - A.det_cap]; };
-  if (lane == 0) {  // initial_state (scheduler.cpp:117-128)
-    BState& s0 = st[0][0];
-    s0.util = 0.0;
-    s0.flex_sum = 0.0;
-    s0.skips = 0;
-    s0.flex_count = 0;
-    s0.free_mask = 0;
-    s0.node = -1;
-    s0.nsurv = 0;
+  const int lgE = E <= 1 ? 0 : 32 - __clz(E - 1);  // engines padded to a power of two
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned le = lt | (1u << lane);
+  int wstatus = 0;
+  // BeamState w lives in lane w (initial_state, scheduler.cpp:117-128)
+  double st_u = 0.0, st_fs = 0.0;
+  int st_fc = 0, st_nd = -1, st_ns = 0, st_lq = -1, st_ln = 0;
+  long long st_sk = 0;
+  uint32_t st_fm = 0;
+  if (lane == 0) {
     for (int e = 0; e < E; ++e) {
       const int occ = A.eng.occ[e];
-      if (occ > A.eng.slots[e]) s_status = AG_ERR_VALIDATION + 200;  // engine over capacity
-      s0.occ[e] = occ;
-      s0.util += occ * A.eng.weight[e];
-      if (A.eng.slots[e] - occ > 0) s0.free_mask |= 1u << e;
+      if (occ > e_slots[e]) wstatus = AG_ERR_VALIDATION + 200;  // engine over capacity
+      s_occ[0][0][e] = occ;
+      st_u += occ * e_weight[e];
+      if (e_slots[e] - occ > 0) st_fm |= 1u << e;
     }
-    lex[0].len[0] = 0;
   }
+  wstatus = __shfl_sync(kFull, wstatus, 0);
   __syncwarp();
-  if (s_status) {
-    if (lane == 0) A.out[0] = s_status;
-    return;
-  }
   int cur = 0, nst = 1, nnodes = 0;
   unsigned long long explored = 1;
-  int pi = 0;       // next pair position not yet accounted for
-  int j = 0;        // next candidate index
-  int last_q = -1;  // request of the last visited candidate
+  long long pi = 0;  // next pair position not yet accounted for
+  int j = 0;         // next candidate index
+  int last_q = -1;   // request of the last visited candidate
+  unsigned have = 0; // candidates known to be published
+  int rows = 0;      // candidates known to have staged histogram rows
   long long tw[4] = {0, 0, 0, 0};
+  unsigned long long n_steps = 0, n_child = 0;
   long long tp = clock64();
-  while (true) {
-    uint32_t U = lane < nst ? st[cur][lane].free_mask : 0u;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) U |= __shfl_xor_sync(0xffffffffu, U, o);
+  // published count once it exceeds idx, or the final count
+  auto wait_for = [&](unsigned idx) -> unsigned {
+    if (idx < have) return have;
+    unsigned v = 0;
+    if (lane == 0) {
+      // relaxed spin, then one acquire of the published count
+      for (;;) {
+        const unsigned done = *(volatile unsigned*)&s_prod_done;
+        v = *(volatile unsigned*)&s_produced;
+        if (v > idx || done) break;
+        __nanosleep(32);
+      }
+      v = ld_acquire(&s_produced);
+      __threadfence_block();
+      if (have == 0 && v && A.timing) A.timing[2] = gtimer();
+    }
+    have = __shfl_sync(kFull, v, 0);
+    return have;
+  };
+  auto maskf = [&](int i) -> uint32_t { return i < A.cand_cap ? c_mask[i] : A.gmask[i - A.cand_cap]; };
+  auto recf = [&](int i) -> Cand { return i < A.cand_cap ? c_rec[i] : A.grec[i - A.cand_cap]; };
+
+  while (!wstatus) {
+    const uint32_t U = __reduce_or_sync(kFull, lane < nst ? st_fm : 0u);
     if (!U) break;  // all-full early exit (scheduler.cpp:303-315)
-    // the next candidate of the current request is visited unconditionally
-    // (a touched state may still have a constrained mask); otherwise the next
-    // candidate whose mask meets a free engine
-    int found = ncand;
-    if (j < ncand && last_q >= 0 && detf(j).qi == last_q) {
+    // the next candidate of the current request is visited unconditionally;
+    // otherwise the next candidate whose mask meets a free engine
+    int found = -1;
+    if (last_q >= 0 && wait_for((unsigned)j) > (unsigned)j && recf(j).qi == last_q) {
       found = j;
     } else {
-      for (int j0 = j; j0 < ncand; j0 += 32) {
+      for (int j0 = j;;) {
+        const unsigned h = wait_for((unsigned)j0);
+        if (h <= (unsigned)j0) break;  // producers done, list exhausted
         const int jj = j0 + lane;
-        const bool ok = jj < ncand && (cmaskf(jj) & U) != 0;
-        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        const bool ok = jj < (int)h && (maskf(jj) & U) != 0;
+        const uint32_t b = __ballot_sync(kFull, ok);
         if (b) {
           found = j0 + __ffs(b) - 1;
           break;
         }
+        j0 = min(j0 + 32, (int)h);
       }
     }
     { const long long t = clock64(); tw[0] += t - tp; tp = t; }
-    if (found >= ncand) break;
+    if (found < 0) break;
     j = found;
-    const int ppos = cposf(j);
+    const Cand cr = recf(j);
     {  // whole-beam skips before this pair
-      const long long k = ppos - pi;
+      const long long k = (long long)cr.pos - pi;
       if (k > 0) {
-        if (lane < nst) st[cur][lane].skips += k;
+        if (lane < nst) st_sk += k;
         explored += (unsigned long long)nst * (unsigned long long)k;
       }
-      pi = ppos + 1;
+      pi = (long long)cr.pos + 1;
     }
-    const Det d = detf(j);
-    const int qcur = d.qi, a = d.agent, slot = d.slot;
-    const uint32_t base = cmaskf(j);
-    const double initial = (double)d.nvia;
-    const bool tch = lane < nst && st[cur][lane].node >= 0 && nv[st[cur][lane].node].qi == qcur;
+    const int qcur = cr.qi, a = (int)(cr.slot_agent >> 26), slot = (int)(cr.slot_agent & 0x3ffffffu);
+    const uint32_t base = maskf(j);
+    const double initial = (double)cr.nvia;
+    const int hrow = j;
+    if (hrow >= rows && hrow < A.hist_cap) rows = ld_acquire(&s_rows);  // uniform
+    const bool tch = lane < nst && st_lq == qcur;
     // allowed_engines (scheduler.cpp:140-156)
-    uint32_t mk = (lane < nst && !tch) ? (base & st[cur][lane].free_mask) : 0u;
-    const uint32_t tmask = __ballot_sync(0xffffffffu, tch);
+    uint32_t mk = (lane < nst && !tch) ? (base & st_fm) : 0u;
+    const uint32_t tmask = __ballot_sync(kFull, tch);
     // re-touch: counts per model of this agent over the request's viable
     // configurations consistent with the state's earlier triples for it
     for (uint32_t tb = tmask; tb; tb &= tb - 1) {
       const int si = __ffs(tb) - 1;
+      const int snode = __shfl_sync(kFull, st_nd, si);
       if (lane == 0) {
-        int n = st[cur][si].node, nc = 0;
+        int n = snode, nc = 0;
         while (n >= 0 && nv[n].qi == qcur) {
           s_cons[nc][0] = nv[n].am >> 8;
           s_cons[nc][1] = nv[n].am & 0xFF;
@@ -507,165 +695,178 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       if (lane == si) {
         uint32_t em = 0;
         for (int mdl = 0; mdl < M; ++mdl)
-          if (s_cnt[si][mdl] > 0) em |= 1u << A.eng.m2e[mdl];
-        mk = em & st[cur][si].free_mask;
+          if (s_cnt[si][mdl] > 0) em |= 1u << e_m2e[mdl];
+        mk = em & st_fm;
       }
       __syncwarp();
     }
     last_q = qcur;
     ++j;
-    const bool has = lane < nst && mk != 0;
-    if (!__any_sync(0xffffffffu, has)) {  // whole-beam skip (scheduler.cpp:317-329)
-      if (lane < nst) st[cur][lane].skips += 1;
+    if (!__any_sync(kFull, lane < nst && mk != 0)) {  // whole-beam skip (scheduler.cpp:317-329)
+      if (lane < nst) st_sk += 1;
       explored += (unsigned long long)nst;
       continue;
     }
     // children in (state, engine ascending) order; a state with no free
-    // candidate contributes one skip child (scheduler.cpp:331-349)
+    // candidate contributes one skip child (scheduler.cpp:331-349).
+    // Exclusive offsets of the per-state child counts (<= 33) by bit slices.
     const int my_n = lane < nst ? (mk ? __popc(mk) : 1) : 0;
-    int xs = my_n;
+    int off = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, xs, o);
-      if (lane >= o) xs += y;
-    }
-    const int nchild = __shfl_sync(0xffffffffu, xs, 31);
-    const int hrow = j - 1;  // this candidate's index
+    for (int bit = 0; bit < 6; ++bit) off += __popc(__ballot_sync(kFull, (my_n >> bit) & 1) & lt) << bit;
+    const int nchild = __shfl_sync(kFull, off + my_n, 31);
     explored += (unsigned long long)nchild;
-    const Lex& L = lex[cur];
+    ++n_steps;
+    n_child += nchild;
+    const uint64_t(*R)[kMaxBeam] = s_rel[cur];
     const uint64_t key_base = tkey(qcur, a, 0);
+    const bool fast = nchild <= 32;
     int npick = 0;
-    if (nchild <= 32) {
-      // lane c builds child c in registers (extend_state, scheduler.cpp:158-206)
-      const int c = lane;
-      int si = 0, off = 0;
-      for (int s2 = 0; s2 < nst; ++s2) {
-        const int o2 = __shfl_sync(0xffffffffu, xs - my_n, s2);
-        if (c >= o2) si = s2, off = o2;
-      }
-      const uint32_t pm = __shfl_sync(0xffffffffu, mk, si);
-      const bool ptch = __shfl_sync(0xffffffffu, (int)tch, si) != 0;
-      double cu = -1.0, cfs = 0.0, cf = 0.0;
-      long long csk = 0;
-      int cfc = 0, cns = 0, ce = -1;
-      uint64_t ck = kEnd;
-      const bool valid = c < nchild;
-      if (valid) {
-        const BState& p = st[cur][si];
-        if (!pm) {
-          cu = p.util;
-          cfs = p.flex_sum;
-          cfc = p.flex_count;
-          csk = p.skips + 1;
-          cns = p.nsurv;
-        } else {
-          ce = __fns(pm, 0, c - off + 1);
-          const int mdl = A.eng.model[ce];
-          cu = p.util + A.eng.weight[ce];
-          csk = p.skips;
-          if (!ptch) {
-            const uint32_t surv = hrow < A.hist_cap ? c_hist[hrow * M + mdl]
-                                                    : __ldg(A.hist + ((size_t)slot * N + a) * M + mdl);
-            cfs = p.flex_sum + (double)surv / initial;
-            cfc = p.flex_count + 1;
-            cns = (int)surv;
+    // the picked child's values (lane w: the child adopted as state w)
+    double c_u = 0.0, c_fs = 0.0;
+    long long c_sk = 0;
+    int c_fc = 0, c_ns = 0, c_par = 0, c_eng = -1;
+    if (fast) {
+      // lane c builds child c (extend_state, scheduler.cpp:158-206)
+      const unsigned starts = __reduce_or_sync(kFull, lane < nst ? (1u << off) : 0u);
+      const unsigned sl = starts & le;
+      const bool valid = lane < nchild;
+      const int par = valid ? __popc(sl) - 1 : 0;
+      const int poff = valid ? 31 - __clz(sl) : 0;
+      const double pu = __shfl_sync(kFull, st_u, par);
+      const double pfs = __shfl_sync(kFull, st_fs, par);
+      const int pfc = __shfl_sync(kFull, st_fc, par);
+      const long long psk = __shfl_sync(kFull, st_sk, par);
+      const int pns = __shfl_sync(kFull, st_ns, par);
+      const uint32_t pm = __shfl_sync(kFull, mk, par);
+      const bool ptch = ((tmask >> par) & 1u) != 0;
+      double cu = pu, cfs = pfs, cf = 1.0;
+      long long csk = psk;
+      int cfc = pfc, cns = pns, ce = -1, cm1 = 0;  // cm1: model + 1, 0 for the skip child
+      if (!pm) {
+        csk = psk + 1;
+      } else {
+        ce = __fns(pm, 0, lane - poff + 1);
+        const int mdl = e_model[ce];
+        cm1 = mdl + 1;
+        cu = pu + e_weight[ce];
+        if (!ptch) {
+          uint32_t surv;
+          double r;
+          if (hrow < rows) {
+            surv = h_cnt[hrow * M + mdl];
+            r = h_rat[hrow * M + mdl];
           } else {
-            const int surv = s_cnt[si][mdl];
-            const double before = (double)p.nsurv / initial;
-            cfs = p.flex_sum + ((double)surv / initial - before);
-            cfc = p.flex_count;
-            cns = surv;
+            surv = __ldg(A.hist + ((size_t)slot * N + a) * M + mdl);
+            r = (double)surv / initial;
           }
-          ck = key_base | (uint64_t)(uint32_t)mdl;
+          cfs = pfs + r;
+          cfc = pfc + 1;
+          cns = (int)surv;
+        } else {
+          const int surv = s_cnt[par][mdl];
+          const double before = (double)pns / initial;
+          cfs = pfs + ((double)surv / initial - before);
+          cns = surv;
         }
-        cf = cfc > 0 ? cfs / cfc : 1.0;
-        Child& chd = children[c];
-        chd.util = cu;
-        chd.flex_sum = cfs;
-        chd.flex = cf;
-        chd.skips = csk;
-        chd.flex_count = cfc;
-        chd.nsurv = cns;
-        chd.parent = (int16_t)si;
-        chd.eng = (int16_t)ce;
       }
-      // warp bitonic sort, best first, under state_better (scheduler.cpp:
-      // 109-115) then the lower child index; only keys move between lanes
-      double ku = cu, kf = cf;
-      long long ks = csk;
-      int kp = si, ki = valid ? c : -1;
-      uint64_t kk = ck;
-#pragma unroll 1
-      for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll 1
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
-          const double ou = __shfl_xor_sync(0xffffffffu, ku, jj);
-          const double of = __shfl_xor_sync(0xffffffffu, kf, jj);
-          const long long os = __shfl_xor_sync(0xffffffffu, ks, jj);
-          const int op = __shfl_xor_sync(0xffffffffu, kp, jj);
-          const int oi = __shfl_xor_sync(0xffffffffu, ki, jj);
-          const uint64_t ok = __shfl_xor_sync(0xffffffffu, kk, jj);
-          bool ob;  // other strictly before mine
-          if (oi < 0) ob = false;
-          else if (ki < 0) ob = true;
-          else if (ou != ku) ob = ou > ku;
-          else if (of != kf) ob = of > kf;
-          else if (os != ks) ob = os < ks;
-          else if (lex_less(L, op, ok, kp, kk)) ob = true;
-          else if (lex_less(L, kp, kk, op, ok)) ob = false;
-          else ob = oi < ki;
-          const bool lo = (lane & jj) == 0, asc = (lane & k) == 0;
-          const bool take = (lo == asc) ? ob : (!ob && oi != ki);
-          if (take) ku = ou, kf = of, ks = os, kp = op, ki = oi, kk = ok;
+      cf = cfc > 0 ? cfs / cfc : 1.0;
+      const uint64_t ku = okey(cu), kf = okey(cf);
+      const uint32_t sk = (uint32_t)csk;
+      const uint64_t ck = cm1 ? key_base | (uint64_t)(cm1 - 1) : kEnd;
+      if (valid) {
+        RankKey rk;
+        rk.ku = ku;
+        rk.kf = kf;
+        rk.sk = sk;
+        rk.pk = (uint32_t)par | ((uint32_t)cm1 << 8);
+        rk.pad = 0;
+        s_rk[lane] = rk;
+      }
+      __syncwarp();
+      { const long long t = clock64(); tw[1] += t - tp; tp = t; }
+      // rank under state_better, then the lower child index (never reached:
+      // distinct children hold distinct lists); batches of 4 with every
+      // shared-memory load issued up front, comparisons branch-free
+      unsigned rank = 0xffffffffu;
+      if (valid) {
+        rank = 0;
+        for (int c0 = 0; c0 < nchild; c0 += 4) {
+          RankKey y[4];
+          uint64_t rr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) y[u] = s_rk[min(c0 + u, 31)];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rr[u] = R[y[u].pk & 31u][par];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int c2 = c0 + u;
+            const uint32_t ym1 = y[u].pk >> 8;
+            const uint64_t yk = ym1 ? key_base | (uint64_t)(ym1 - 1) : kEnd;
+            const bool lexb = lex_before((int)(y[u].pk & 31u) == par, rr[u], yk, ck);
+            const bool yb = (y[u].ku > ku) |
+                            ((y[u].ku == ku) & ((y[u].kf > kf) | ((y[u].kf == kf) & ((y[u].sk < sk) |
+                                                                                     ((y[u].sk == sk) & lexb)))));
+            rank += (c2 < nchild) & (c2 != lane) & yb;
+          }
         }
       }
       // nested retention (scheduler.cpp:351-370): level w adopts the best
-      // unused child of parents < w -- the first eligible in sorted order
-      uint32_t used = 0;
-      for (int w = 1; w <= B; ++w) {
-        const uint32_t el = __ballot_sync(0xffffffffu, ki >= 0 && kp < w) & ~used;
-        if (!el) continue;
-        const int src = __ffs(el) - 1;
-        used |= 1u << src;
-        const int pc = __shfl_sync(0xffffffffu, ki, src);
-        if (lane == 0) s_picked[npick] = pc;
+      // unused child of parents < w
+      bool used = false;
+      for (int w = 1; w <= B && npick < nchild; ++w) {
+        const bool el = valid && !used && par < w;
+        const unsigned m = __reduce_min_sync(kFull, el ? rank : 0xffffffffu);
+        if (m == 0xffffffffu) continue;
+        if (el && rank == m) {
+          used = true;
+          s_picked[npick] = lane;
+        }
         ++npick;
       }
+      __syncwarp();
+      const int src = lane < npick ? s_picked[lane] : 0;
+      c_u = __shfl_sync(kFull, cu, src);
+      c_fs = __shfl_sync(kFull, cfs, src);
+      c_fc = __shfl_sync(kFull, cfc, src);
+      c_sk = __shfl_sync(kFull, csk, src);
+      c_ns = __shfl_sync(kFull, cns, src);
+      c_par = __shfl_sync(kFull, par, src);
+      c_eng = __shfl_sync(kFull, ce, src);
     } else {
-      // wide beams: children through shared memory, per level a warp arg-max
+      // wide beams: lane w writes its children, per level a warp arg-max
       if (lane < nst) {
-        const BState& p = st[cur][lane];
-        int c = xs - my_n;
+        int c = off;
         if (!mk) {
           Child& chd = children[c];
           chd.parent = (int16_t)lane;
           chd.eng = -1;
-          chd.util = p.util;
-          chd.flex_sum = p.flex_sum;
-          chd.flex_count = p.flex_count;
-          chd.skips = p.skips + 1;
-          chd.nsurv = p.nsurv;
-          chd.flex = chd.flex_count > 0 ? chd.flex_sum / chd.flex_count : 1.0;
+          chd.util = st_u;
+          chd.flex_sum = st_fs;
+          chd.flex_count = st_fc;
+          chd.skips = st_sk + 1;
+          chd.nsurv = st_ns;
+          chd.flex = st_fc > 0 ? st_fs / st_fc : 1.0;
         } else {
           for (uint32_t b = mk; b; b &= b - 1, ++c) {
             const int e = __ffs(b) - 1;
-            const int mdl = A.eng.model[e];
+            const int mdl = e_model[e];
             Child& chd = children[c];
             chd.parent = (int16_t)lane;
             chd.eng = (int16_t)e;
-            chd.util = p.util + A.eng.weight[e];
-            chd.skips = p.skips;
+            chd.util = st_u + e_weight[e];
+            chd.skips = st_sk;
             if (!tch) {
-              const uint32_t surv = hrow < A.hist_cap ? c_hist[hrow * M + mdl]
-                                                      : A.hist[((size_t)slot * N + a) * M + mdl];
-              chd.flex_sum = p.flex_sum + (double)surv / initial;
-              chd.flex_count = p.flex_count + 1;
+              const uint32_t surv = hrow < rows ? h_cnt[hrow * M + mdl]
+                                                : A.hist[((size_t)slot * N + a) * M + mdl];
+              chd.flex_sum = st_fs + (hrow < rows ? h_rat[hrow * M + mdl] : (double)surv / initial);
+              chd.flex_count = st_fc + 1;
               chd.nsurv = (int)surv;
             } else {
               const int surv = s_cnt[lane][mdl];
-              const double before = (double)p.nsurv / initial;
-              chd.flex_sum = p.flex_sum + ((double)surv / initial - before);
-              chd.flex_count = p.flex_count;
+              const double before = (double)st_ns / initial;
+              chd.flex_sum = st_fs + ((double)surv / initial - before);
+              chd.flex_count = st_fc;
               chd.nsurv = surv;
             }
             chd.flex = chd.flex_count > 0 ? chd.flex_sum / chd.flex_count : 1.0;
@@ -673,142 +874,176 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         }
       }
       __syncwarp();
-      const WalkCtx wc{children, &lex[cur], key_base, &A.eng};
-      uint32_t used[(kMaxBeam * (kMaxEng + 1) + 31) / 32];
-      for (int i = 0; i < (nchild + 31) / 32; ++i) used[i] = 0;
+      { const long long t = clock64(); tw[1] += t - tp; tp = t; }
+      auto keyf = [&](int c) -> uint64_t {
+        return children[c].eng >= 0 ? key_base | (uint64_t)(uint32_t)e_model[children[c].eng] : kEnd;
+      };
+      auto before = [&](int c1, int c2) -> bool {  // c1 strictly before c2
+        if (c1 < 0) return false;
+        if (c2 < 0) return true;
+        const Child &x = children[c1], &y = children[c2];
+        if (x.util != y.util) return x.util > y.util;
+        if (x.flex != y.flex) return x.flex > y.flex;
+        if (x.skips != y.skips) return x.skips < y.skips;
+        const uint64_t k1 = keyf(c1), k2 = keyf(c2);
+        if (x.parent == y.parent && k1 == k2) return c1 < c2;
+        return rel_before(rel_extend(x.parent == y.parent, R[x.parent][y.parent], k1, k2));
+      };
+      constexpr int kUsedWords = (kMaxBeam * (kMaxEng + 1) + 31) / 32;
+      uint32_t used[kUsedWords];
+      for (int i = 0; i < kUsedWords; ++i) used[i] = 0;
       for (int w = 1; w <= B; ++w) {
         int best = -1;
         for (int c = lane; c < nchild; c += 32) {
           if ((used[c >> 5] >> (c & 31)) & 1u) continue;
           if (children[c].parent >= w) continue;
-          if (wc.before(c, best)) best = c;
+          if (before(c, best)) best = c;
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-          const int other = __shfl_xor_sync(0xffffffffu, best, o);
-          if (wc.before(other, best)) best = other;
+          const int other = __shfl_xor_sync(kFull, best, o);
+          if (before(other, best)) best = other;
         }
         if (best < 0) continue;
         used[best >> 5] |= 1u << (best & 31);
         if (lane == 0) s_picked[npick] = best;
         ++npick;
       }
+      __syncwarp();
+      if (lane < npick) {
+        const Child& chd = children[s_picked[lane]];
+        c_u = chd.util;
+        c_fs = chd.flex_sum;
+        c_fc = chd.flex_count;
+        c_sk = chd.skips;
+        c_ns = chd.nsurv;
+        c_par = chd.parent;
+        c_eng = chd.eng;
+      }
     }
-    __syncwarp();
-    { const long long t = clock64(); tw[1] += t - tp; tp = t; }
+    { const long long t = clock64(); tw[2] += t - tp; tp = t; }
     // adopt: picked child w becomes state w of the next beam
     const int nxt = cur ^ 1;
-    bool mknode = false;
-    int pc = -1;
-    if (lane < npick) {
-      pc = s_picked[lane];
-      mknode = children[pc].eng >= 0;
+    const bool mine = lane < npick;
+    if (!mine) c_par = 0, c_eng = -1;
+    const uint32_t p_fm = __shfl_sync(kFull, st_fm, c_par);
+    const int p_nd = __shfl_sync(kFull, st_nd, c_par);
+    const int p_lq = __shfl_sync(kFull, st_lq, c_par);
+    const int p_ln = __shfl_sync(kFull, st_ln, c_par);
+    const bool mknode = c_eng >= 0;
+    const uint32_t nb = __ballot_sync(kFull, mknode);
+    const int c_mdl = mknode ? e_model[c_eng] : 0;
+    const uint64_t mykey = mknode ? key_base | (uint64_t)(uint32_t)c_mdl : kEnd;
+    // occupancy rows of the new states: lane (w, e) copies engine e of state w
+    for (int i0 = 0; i0 < (npick << lgE); i0 += 32) {
+      const int i = i0 + lane, w = min(i >> lgE, 31), e = i & ((1 << lgE) - 1);
+      const int pw = __shfl_sync(kFull, c_par, w);
+      const int ew = __shfl_sync(kFull, c_eng, w);
+      if (w < npick && e < E) s_occ[nxt][w][e] = s_occ[cur][pw][e] + (e == ew ? 1 : 0);
     }
-    const uint32_t nb = __ballot_sync(0xffffffffu, mknode);
-    if (lane < npick) {
-      const Child& chd = children[pc];
-      const BState& p = st[cur][chd.parent];
-      BState& q = st[nxt][lane];
-      for (int e = 0; e < E; ++e) q.occ[e] = p.occ[e];
-      q.util = chd.util;
-      q.flex_sum = chd.flex_sum;
-      q.flex_count = chd.flex_count;
-      q.skips = chd.skips;
-      q.free_mask = p.free_mask;
-      q.node = p.node;
-      q.nsurv = chd.nsurv;
-      lex[nxt].len[lane] = L.len[chd.parent] + (mknode ? 1 : 0);
+    if (mine) {
+      st_u = c_u;
+      st_fs = c_fs;
+      st_fc = c_fc;
+      st_sk = c_sk;
+      st_ns = c_ns;
+      st_fm = p_fm;
       if (mknode) {
-        const int e = chd.eng;
-        if (++q.occ[e] >= A.eng.slots[e]) q.free_mask &= ~(1u << e);
-        const int id = nnodes + __popc(nb & ((1u << lane) - 1u));
+        if (s_occ[cur][c_par][c_eng] + 1 >= e_slots[c_eng]) st_fm &= ~(1u << c_eng);
+        const int id = nnodes + __popc(nb & lt);
         if (id < A.max_nodes) {
           Node nd;
           nd.qi = qcur;
-          nd.am = (a << 8) | A.eng.model[e];
-          nd.prev = p.node;
-          nd.depth = depth_of(nv, p.node) + 1;
-          nd.nsurv = chd.nsurv;
-          nd.nvia = d.nvia;
+          nd.am = (a << 8) | c_mdl;
+          nd.prev = p_nd;
+          nd.depth = p_ln + 1;
+          nd.nsurv = c_ns;
+          nd.nvia = cr.nvia;
           nd.slot = slot;
           nd.pad = 0;
           if (id < kSmemNodes) s_nodes[id] = nd;
           else A.gnodes[id - kSmemNodes] = nd;
         } else {
-          s_status = AG_ERR_INTERNAL + 300;  // history overflow
+          wstatus = AG_ERR_INTERNAL + 300;  // history overflow
         }
-        q.node = id;
+        st_nd = id;
+        st_lq = qcur;
+        st_ln = p_ln + 1;
+      } else {
+        st_nd = p_nd;
+        st_lq = p_lq;
+        st_ln = p_ln;
       }
     }
-    // lexicographic structure of the new beam
-    for (int pr = lane; pr < npick * npick; pr += 32) {
-      const int w1 = pr / npick, w2 = pr - w1 * npick;
-      if (w1 == w2) continue;
-      const Child& c1 = children[s_picked[w1]];
-      const int p1 = c1.parent, p2 = children[s_picked[w2]].parent;
-      const uint64_t k1 = c1.eng >= 0 ? key_base | (uint64_t)(uint32_t)A.eng.model[c1.eng] : kEnd;
-      int l;
-      uint64_t nx;
-      if (p1 == p2) {
-        l = L.len[p1];
-        nx = k1;
-      } else {
-        l = L.lcp[p1][p2];
-        nx = l < L.len[p1] ? L.nxt[p1][p2] : k1;
+    // triples_less relation of the new beam: lane (w1, w2) per ordered pair
+    {
+      const int lgP = npick <= 1 ? 0 : 32 - __clz(npick - 1);
+      for (int i0 = 0; i0 < (1 << (2 * lgP)); i0 += 32) {
+        const int i = i0 + lane, w1 = min(i >> lgP, 31), w2 = i & ((1 << lgP) - 1);
+        const int p1 = __shfl_sync(kFull, c_par, w1), p2 = __shfl_sync(kFull, c_par, w2);
+        const uint64_t k1 = __shfl_sync(kFull, mykey, w1), k2 = __shfl_sync(kFull, mykey, w2);
+        if (w1 < npick && w2 < npick && w1 != w2)
+          s_rel[nxt][w1][w2] = rel_extend_sel(p1 == p2, R[p1][p2], k1, k2);
       }
-      lex[nxt].lcp[w1][w2] = l;
-      lex[nxt].nxt[w1][w2] = nx;
     }
     nnodes += __popc(nb);
-    { const long long t = clock64(); tw[2] += t - tp; tp = t; }
-
+    wstatus = (int)__reduce_max_sync(kFull, (unsigned)wstatus);
     __syncwarp();
-    if (s_status) {
-      if (lane == 0) A.out[0] = s_status;
-      return;
-    }
     cur = nxt;
     nst = npick;
     { const long long t = clock64(); tw[3] += t - tp; tp = t; }
   }
-  if (lane == 0 && A.timing)
-    #pragma unroll
+  // producers stop at their next chunk boundary
+  if (lane == 0) *(volatile unsigned*)&s_walk_done = 1u;
+  if (lane == 0 && A.timing) {
+#pragma unroll
     for (int k = 0; k < 4; ++k) A.timing[5 + k] = (unsigned long long)tw[k];
+    A.timing[9] = n_steps;
+    A.timing[10] = n_child;
+    A.timing[3] = gtimer();
+  }
+  // RoundContext validation covers every pair: wait for the full scan
+  if (check_all) {
+    if (lane == 0)
+      while (!ld_acquire(&s_prod_done)) {
+      }
+    __syncwarp();
+    if (s_status) wstatus = s_status;
+  }
+  if (wstatus) {
+    if (lane == 0) A.out[0] = wstatus;
+    return;
+  }
   {  // the remaining pairs are skips (all-full exit or no candidate left)
-    const long long rem = npairs - pi;
+    const long long rem = A.npairs - pi;
     if (rem > 0) {
-      if (lane < nst) st[cur][lane].skips += rem;
+      if (lane < nst) st_sk += rem;
       explored += (unsigned long long)nst * (unsigned long long)rem;
     }
   }
-  __syncwarp();
-  if (lane == 0 && A.timing) A.timing[3] = gtimer();
 
-  // ---- C: winner and finalize (scheduler.cpp:373-377, 208-220, 248-287)
+  // ---- winner and finalize (scheduler.cpp:373-377, 208-220, 248-287)
+  const uint64_t(*R)[kMaxBeam] = s_rel[cur];
+  double bu = st_u, bf = st_fc > 0 ? st_fs / st_fc : 1.0;
+  long long bsk = st_sk;
   int best = lane < nst ? lane : -1;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    const int other = __shfl_xor_sync(0xffffffffu, best, o);
+    const double ou = __shfl_xor_sync(kFull, bu, o);
+    const double of = __shfl_xor_sync(kFull, bf, o);
+    const long long os = __shfl_xor_sync(kFull, bsk, o);
+    const int other = __shfl_xor_sync(kFull, best, o);
     if (other < 0) continue;
-    if (best < 0) {
-      best = other;
-      continue;
-    }
-    const BState& s1 = st[cur][best];
-    const BState& s2 = st[cur][other];
-    const double f1 = s1.flex_count > 0 ? s1.flex_sum / s1.flex_count : 1.0;
-    const double f2 = s2.flex_count > 0 ? s2.flex_sum / s2.flex_count : 1.0;
     bool o_better;  // is `other` strictly better than `best`?
-    if (s1.util != s2.util) o_better = s2.util > s1.util;
-    else if (f1 != f2) o_better = f2 > f1;
-    else if (s1.skips != s2.skips) o_better = s2.skips < s1.skips;
-    else if (lex_less(lex[cur], other, kEnd, best, kEnd)) o_better = true;
-    else if (lex_less(lex[cur], best, kEnd, other, kEnd)) o_better = false;
-    else o_better = other < best;
-    if (o_better) best = other;
+    if (best < 0) o_better = true;
+    else if (ou != bu) o_better = ou > bu;
+    else if (of != bf) o_better = of > bf;
+    else if (os != bsk) o_better = os < bsk;
+    else o_better = rel_before(R[other][best]);
+    if (o_better) best = other, bu = ou, bf = of, bsk = os;
   }
-  const BState& w = st[cur][best];
-  const int D = depth_of(nv, w.node);
+  const int w_nd = __shfl_sync(kFull, st_nd, best);
+  const int D = __shfl_sync(kFull, st_ln, best);
   ag_assignment* res = reinterpret_cast<ag_assignment*>((char*)A.out + kOutHeader);
   int32_t* occ_out = reinterpret_cast<int32_t*>(res + 1);
   ag_triple* triples = reinterpret_cast<ag_triple*>(occ_out + kMaxEng);
@@ -821,119 +1056,102 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   }
   // the path, root first (node ids into the children area, free now)
   int* path = reinterpret_cast<int*>(children);
-  int path_cap = (int)(sizeof(Child) * A.max_children / sizeof(int));
+  const int path_cap = (int)(sizeof(Child) * A.max_children / sizeof(int));
   if (lane == 0) {
-    int n = w.node;
+    int n = w_nd;
     for (int i = D - 1; i >= 0; --i) {
       if (i < path_cap) path[i] = n;
       n = nv[n].prev;
     }
   }
   __syncwarp();
-  for (int i = lane; i < D; i += 32) {
+  double* fr = reinterpret_cast<double*>(s_cnt);  // per-request ratios (<= 512)
+  bool ascending = D <= path_cap;
+  for (int i0 = 0; i0 < D; i0 += 32) {
+    const int i = i0 + lane;
     int n = -1;
-    if (i < path_cap) {
-      n = path[i];
-    } else {  // long path: walk from the winner (rare)
-      n = w.node;
-      for (int k = D - 1; k > i; --k) n = nv[n].prev;
+    if (i < D) {
+      if (i < path_cap) {
+        n = path[i];
+      } else {  // long path: walk from the winner (rare)
+        n = w_nd;
+        for (int k = D - 1; k > i; --k) n = nv[n].prev;
+      }
+      const Node nd = nv[n];
+      ag_triple t;
+      t.request_index = nd.qi;
+      t.agent = nd.am >> 8;
+      t.model = nd.am & 0xFF;
+      t.slot = nd.slot;
+      t.request_id = A.ids[nd.slot];
+      triples[i] = t;
     }
-    const Node nd = nv[n];
-    ag_triple t;
-    t.request_index = nd.qi;
-    t.agent = nd.am >> 8;
-    t.model = nd.am & 0xFF;
-    t.slot = nd.slot;
-    t.request_id = A.ids[nd.slot];
-    triples[i] = t;
+    if (ascending) {
+      // a request's triples are consecutive on the path; in a session the
+      // queue is in FIFO = container order, so requests appear ascending
+      const bool viol = i + 1 < D && nv[n].qi > nv[path[i + 1]].qi;
+      if (__any_sync(kFull, viol)) ascending = false;
+    }
   }
   __syncwarp();
+  double flex_sum = 0.0;
+  int flex_count = 0;
+  if (D > 0 && ascending && D <= (int)(sizeof(s_cnt) / sizeof(double))) {
+    // the last triple of each request carries its survivors; fold in order
+    for (int i = lane; i < D; i += 32) {
+      const Node& nd = nv[path[i]];
+      const bool last = i + 1 == D || nv[path[i + 1]].qi != nd.qi;
+      fr[i] = last ? (double)nd.nsurv / (double)nd.nvia : -1.0;
+    }
+    __syncwarp();
+    if (lane == 0)
+      for (int i = 0; i < D; ++i)
+        if (fr[i] >= 0.0) {
+          flex_sum += fr[i];
+          ++flex_count;
+        }
+  } else if (D > 0 && lane == 0) {
+    // general container order: repeatedly take the smallest unseen request
+    int prev = -1;
+    for (;;) {
+      int nq = 0x7fffffff;
+      for (int i = 0; i < D; ++i) {
+        const int q = triples[i].request_index;
+        if (q > prev && q < nq) nq = q;
+      }
+      if (nq == 0x7fffffff) break;
+      for (int nn = w_nd; nn >= 0; nn = nv[nn].prev)
+        if (nv[nn].qi == nq) {
+          flex_sum += (double)nv[nn].nsurv / (double)nv[nn].nvia;
+          ++flex_count;
+          break;
+        }
+      prev = nq;
+    }
+  }
   if (lane != 0) return;
-  // score_assignment (scheduler.cpp:248-287): utilization in engine order;
-  // flexibility over touched requests in queue (container) order with the
-  // survivors consistent with all of a request's triples (its last node)
+  // score_assignment: utilization in engine order
   double util = 0.0;
   for (int e = 0; e < E; ++e) {
-    if (w.occ[e] < 0 || w.occ[e] > A.eng.slots[e]) {
+    const int o = s_occ[cur][best][e];
+    if (o < 0 || o > e_slots[e]) {
       A.out[0] = AG_ERR_VALIDATION + 500;
       return;
     }
-    util += w.occ[e] * A.eng.weight[e];
-    occ_out[e] = w.occ[e];
-  }
-  double flex_sum = 0.0;
-  int flex_count = 0;
-  if (D > 0) {
-    // a request's triples are consecutive on the path; in a session the
-    // queue is in FIFO = container order, so requests appear ascending
-    bool ascending = D <= path_cap;
-    int prevq = -1;
-    for (int i = 0; i < D && ascending; ++i) {
-      const int q = nv[path[i]].qi;
-      if (q != prevq) {
-        if (q < prevq) ascending = false;
-        prevq = q;
-      }
-    }
-    if (ascending) {
-      int n = w.node, lastq = -1;
-      // walk back: the first node met per request is its last triple; fold
-      // order must be ascending, so accumulate into a stack then fold
-      int* stk = path + min(D, path_cap);  // reuse space after the path
-      int ns = 0;
-      const int stk_cap = path_cap - min(D, path_cap);
-      bool spill = false;
-      while (n >= 0) {
-        const Node& nd = nv[n];
-        if (nd.qi != lastq) {
-          if (ns < stk_cap) stk[ns] = n;
-          else spill = true;
-          ++ns;
-          lastq = nd.qi;
-        }
-        n = nd.prev;
-      }
-      if (!spill) {
-        for (int k = ns - 1; k >= 0; --k) {
-          const Node& nd = nv[stk[k]];
-          flex_sum += (double)nd.nsurv / (double)nd.nvia;
-          ++flex_count;
-        }
-      } else {
-        ascending = false;  // fall through to the general fold
-      }
-    }
-    if (!ascending) {
-      // general container order: repeatedly take the smallest unseen request
-      int prev = -1;
-      for (;;) {
-        int nq = 0x7fffffff;
-        for (int i = 0; i < D; ++i) {
-          const int q = triples[i].request_index;
-          if (q > prev && q < nq) nq = q;
-        }
-        if (nq == 0x7fffffff) break;
-        for (int nn = w.node; nn >= 0; nn = nv[nn].prev)
-          if (nv[nn].qi == nq) {
-            flex_sum += (double)nv[nn].nsurv / (double)nv[nn].nvia;
-            ++flex_count;
-            break;
-          }
-        prev = nq;
-      }
-    }
+    util += o * e_weight[e];
+    occ_out[e] = o;
   }
   ag_assignment r;
   r.n_triples = D;
   r.pad = 0;
   r.utilization = util;
   r.flexibility = flex_count > 0 ? flex_sum / flex_count : 1.0;
-  r.skips = w.skips;
+  r.skips = bsk;
   r.states_explored = explored;
   *res = r;
   if (A.timing) A.timing[4] = gtimer();
+  A.out[1] = 0;
   A.out[0] = 0;
-  A.out[1] = nreq;
 }
 
 // ------------------------------------------------------------ prune kernel
@@ -953,6 +1171,7 @@ struct PruneArgs {
   uint64_t place_magic[kMaxAgents];
   uint64_t div_m;
   int32_t* status;
+  uint32_t* ever;  // OR of every installed candidate-model mask (round validation)
 };
 
 __device__ __forceinline__ uint32_t digit_p(uint32_t c, int a, const PruneArgs& A) {
@@ -1040,6 +1259,7 @@ __global__ void __launch_bounds__(256) k_sched_prune(PruneArgs A) {
     for (int mdl = 0; mdl < A.M; ++mdl)
       if (s_hist[tid * A.M + mdl]) cm |= 1u << mdl;
     A.cand[(size_t)s * A.N + tid] = cm;
+    if (A.g_meta) atomicOr(A.ever, cm);
   }
   if (tid == 0) A.nviable[s] = len;
 }
@@ -1092,6 +1312,9 @@ struct ag_sched {
   size_t dead = 0;
   std::vector<int32_t> upd_slot;
   std::vector<uint64_t> upd_mask;
+  long long npairs = 0;  // ready pairs over live slots (sum of popcount(ready))
+  std::vector<uint32_t> seen;  // update dedup stamps
+  uint32_t seen_stamp = 0;
   int8_t prio[64];
   uint32_t place[agb::kMaxAgents];
   uint64_t place_magic[agb::kMaxAgents];
@@ -1099,7 +1322,7 @@ struct ag_sched {
   double last_round_us = 0.0;
   // device
   agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx;
-  agb::Scratch d_cpos, d_cmask, d_det, d_nodes, d_out, d_status, d_upd, d_gam, d_qa;
+  agb::Scratch d_cpos, d_det, d_nodes, d_status, d_gam, d_qa, d_upd;  // d_cpos / d_det: candidate overflow
   // pinned host staging
   void* h_res = nullptr;
   size_t h_res_bytes = 0;
@@ -1107,10 +1330,18 @@ struct ag_sched {
   size_t h_stage_bytes = 0;
   void* h_rstage = nullptr;  // round uploads
   size_t h_rstage_bytes = 0;
+  // device views of the mapped buffers (refreshed when reallocated)
+  void* h_rstage_mapped = nullptr;
+  void* h_res_mapped = nullptr;
+  char* h_rstage_dev = nullptr;
+  int32_t* h_res_dev = nullptr;
+  void* h_ostage = nullptr;  // FIFO re-uploads after a compaction
+  size_t h_ostage_bytes = 0;
   ~ag_sched() {
     if (h_res) cudaFreeHost(h_res);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_rstage) cudaFreeHost(h_rstage);
+    if (h_ostage) cudaFreeHost(h_ostage);
   }
 };
 
@@ -1123,9 +1354,26 @@ int ensure_pinned(void** p, size_t* have, size_t bytes) {
   if (*p) cudaFreeHost(*p);
   *p = nullptr;
   *have = 0;
-  AG_CUDA(cudaMallocHost(p, b));
+  AG_CUDA(cudaHostAlloc(p, b, cudaHostAllocMapped));
   *have = b;
   return AG_OK;
+}
+
+// device view of mapped pinned memory
+template <typename T>
+int dev_ptr(void* host, T** out) {
+  void* d = nullptr;
+  AG_CUDA(cudaHostGetDevicePointer(&d, host, 0));
+  *out = reinterpret_cast<T*>(d);
+  return AG_OK;
+}
+
+// the host mirror of Request::ready_agents and the queue's pair count
+void set_ready(ag_sched* s, int slot, uint64_t r) {
+  s->npairs += (long long)__builtin_popcountll(r) - (long long)__builtin_popcountll(s->ready[slot]);
+  s->ready[slot] = r;
+  s->upd_slot.push_back(slot);
+  s->upd_mask.push_back(r);
 }
 
 uint64_t ready_of(const ag_sched* s, int slot) {
@@ -1150,6 +1398,23 @@ void compact_order(ag_sched* s) {
   s->dead = 0;
   s->free_slots.insert(s->free_slots.end(), s->quarantine.begin(), s->quarantine.end());
   s->quarantine.clear();
+}
+
+// A long dirty FIFO tail (after a compaction or a large add) is copied now,
+// outside the next round's decision latency.
+int flush_order(ag_sched* s) {
+  const size_t Q = s->order.size();
+  if (Q <= s->dirty_from || Q - s->dirty_from < 4096) return AG_OK;
+  const size_t n = Q - s->dirty_from;
+  // the staging buffer may still be in use by an earlier async copy
+  AG_CUDA(cudaStreamSynchronize(s->ctx->stream));
+  int rc = ensure_pinned(&s->h_ostage, &s->h_ostage_bytes, n * 4);
+  if (rc) return rc;
+  std::memcpy(s->h_ostage, s->order.data() + s->dirty_from, n * 4);
+  AG_CUDA(cudaMemcpyAsync((int32_t*)s->d_order.p + s->dirty_from, s->h_ostage, n * 4, cudaMemcpyHostToDevice,
+                          s->ctx->stream));
+  s->dirty_from = Q;
+  return AG_OK;
 }
 
 int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vector<int32_t>& g_begin,
@@ -1190,6 +1455,7 @@ int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vec
   std::memcpy(A.place_magic, s->place_magic, sizeof A.place_magic);
   A.div_m = ctx->space->dev().div_m;
   A.status = (int32_t*)s->d_status.p;
+  A.ever = (uint32_t*)((char*)s->d_status.p + 8);
   {
     Launch L(ctx, meta ? K_SCHED_PREP : K_SCHED_APPLY);
     k_sched_prune<<<G, 256, 0, ctx->stream>>>(A);
@@ -1224,6 +1490,8 @@ int engines_dev(const ag_engines* e, EngDev* out) {
 }
 
 // One round over the session queue (or an explicit FIFO/container mapping).
+constexpr size_t kMappedMax = 32 * 1024;  // round deltas read over PCIe by the kernel
+
 int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx_host,
               ag_assignment* out, ag_triple* triples, int32_t triples_cap, int32_t* occupancy) {
   const auto t_start = std::chrono::steady_clock::now();
@@ -1240,15 +1508,15 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   const int max_children = B * (ed.E + 1);
   const size_t max_pairs = (size_t)Q * (size_t)s->N + 1;
   const int max_nodes = (int)std::min<size_t>((size_t)B * max_pairs + 16, (size_t)1 << 30);
-  // ---- uploads: order tail, ready updates (deduplicated: one entry per slot)
-  cudaStream_t st = ctx->stream;
+  // ---- ready updates (deduplicated: the last one per slot wins)
   if (s->upd_slot.size() > 1) {
-    std::vector<char> seen(s->cap, 0);
+    if (s->seen.size() != (size_t)s->cap) s->seen.assign(s->cap, 0);
+    const uint32_t stamp = ++s->seen_stamp;
     size_t w = s->upd_slot.size();
     for (size_t i = s->upd_slot.size(); i-- > 0;) {
       const int slot = s->upd_slot[i];
-      if (seen[slot]) continue;
-      seen[slot] = 1;
+      if (s->seen[slot] == stamp) continue;
+      s->seen[slot] = stamp;
       --w;
       s->upd_slot[w] = slot;
       s->upd_mask[w] = s->upd_mask[i];
@@ -1257,48 +1525,59 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
     s->upd_mask.erase(s->upd_mask.begin(), s->upd_mask.begin() + w);
   }
   const size_t nu = s->upd_slot.size();
-  const size_t n_tail = Q > (int)s->dirty_from ? Q - s->dirty_from : 0;
-  const size_t up_bytes = nu * 12 + 16 + n_tail * 4 + (cidx_host ? (size_t)Q * 4 : 0);
+  const size_t tail_from = std::min<size_t>(s->dirty_from, (size_t)Q);
+  const size_t n_tail = Q - tail_from;
+  // mapped staging: masks | slots | FIFO tail | container indices
+  const size_t off_slot = nu * 8;
+  const size_t off_tail = off_slot + nu * 4;
+  const size_t off_cidx = off_tail + n_tail * 4;
+  const size_t up_bytes = off_cidx + (cidx_host ? (size_t)Q * 4 : 0) + 16;
   const size_t res_bytes = kOutHeader + sizeof(ag_assignment) + 4 * kMaxEng + (size_t)cap_t * sizeof(ag_triple);
   if ((rc = ensure_pinned(&s->h_rstage, &s->h_rstage_bytes, up_bytes)) ||
-      (rc = ensure_pinned(&s->h_res, &s->h_res_bytes, res_bytes)) ||
-      (rc = s->d_upd.ensure(up_bytes)) ||
-      (rc = s->d_out.ensure(res_bytes)) || (rc = s->d_status.ensure(192)))
+      (rc = ensure_pinned(&s->h_res, &s->h_res_bytes, res_bytes)) || (rc = s->d_status.ensure(192)) ||
+      (rc = s->d_cidx.ensure(cidx_host ? (size_t)Q * 4 : 4)))
     return rc;
-  // the previous round synchronised after its last use of h_rstage
+  // the previous round synchronised after its last use of h_rstage / h_res
   char* h = (char*)s->h_rstage;
   std::memcpy(h, s->upd_mask.data(), nu * 8);
-  std::memcpy(h + nu * 8, s->upd_slot.data(), nu * 4);
-  const size_t off_cidx = (nu * 12 + 15) & ~(size_t)15;
+  std::memcpy(h + off_slot, s->upd_slot.data(), nu * 4);
+  std::memcpy(h + off_tail, s->order.data() + tail_from, n_tail * 4);
   if (cidx_host) std::memcpy(h + off_cidx, cidx_host, (size_t)Q * 4);
-  const size_t up_main = off_cidx + (cidx_host ? (size_t)Q * 4 : 0);
-  if (up_main) AG_CUDA(cudaMemcpyAsync(s->d_upd.p, h, up_main, cudaMemcpyHostToDevice, st));
-  if (n_tail) {
-    std::memcpy(h + up_main, s->order.data() + s->dirty_from, n_tail * 4);
-    AG_CUDA(cudaMemcpyAsync((int32_t*)s->d_order.p + s->dirty_from, h + up_main, n_tail * 4,
-                            cudaMemcpyHostToDevice, st));
-    s->dirty_from = Q;
+  if (s->h_rstage != s->h_rstage_mapped) {
+    if ((rc = dev_ptr(s->h_rstage, &s->h_rstage_dev))) return rc;
+    s->h_rstage_mapped = s->h_rstage;
   }
-  // ---- shared memory plan: nodes | children | cand (pos, mask) | details | hist rows
-  const size_t static_bytes = 2 * kMaxBeam * sizeof(BState) + 2 * sizeof(Lex) + kMaxBeam * 32 * 4 + 8192;
+  if (s->h_res != s->h_res_mapped) {
+    if ((rc = dev_ptr(s->h_res, &s->h_res_dev))) return rc;
+    s->h_res_mapped = s->h_res;
+  }
+  char* hd = s->h_rstage_dev;
+  int32_t* out_d = s->h_res_dev;
+  if (up_bytes > kMappedMax) {
+    // large deltas (a fresh session): one DMA copy instead of PCIe reads
+    if ((rc = s->d_upd.ensure(up_bytes))) return rc;
+    AG_CUDA(cudaMemcpyAsync(s->d_upd.p, h, up_bytes, cudaMemcpyHostToDevice, ctx->stream));
+    hd = (char*)s->d_upd.p;
+  }
+  // ---- shared memory plan: nodes | children | ratio rows | cand records |
+  // cand masks | count rows
+  const size_t static_bytes = sizeof(int) * 2 * kMaxBeam * kMaxEng + 2 * 8 * kMaxBeam * kMaxBeam +
+                              sizeof(RankKey) * 32 + kMaxBeam * 32 * 4 + 4 * 1024 + 4096;
   const size_t max_dyn = 227 * 1024 - static_bytes;
   const size_t fixed = sizeof(Node) * kSmemNodes + sizeof(Child) * (size_t)max_children;
   if (fixed > max_dyn) return fail(AG_ERR_VALIDATION, "beam too wide for one CTA");
   size_t room = max_dyn - fixed;
-  const int cand_cap = (int)std::min<size_t>(max_pairs, room * 5 / 10 / 8);
-  room -= (size_t)cand_cap * 8;
-  // the walk visits the head of the candidate list (engines fill quickly);
-  // details and histogram rows are staged for that head only
-  const int det_cap = (int)std::min<size_t>(std::min<size_t>(max_pairs, 2048), room / 2 / sizeof(Det));
-  room -= (size_t)det_cap * sizeof(Det);
-  const int hist_cap =
-      (int)std::min<size_t>(std::min<size_t>((size_t)det_cap, 512), room / (4 * (size_t)s->M));
-  const size_t dyn = fixed + (size_t)cand_cap * 8 + (size_t)det_cap * sizeof(Det) +
-                     (size_t)hist_cap * 4 * s->M;
+  // the walk visits the head of the candidate list (engines fill quickly):
+  // histogram rows and ratios are staged for that head only
+  const size_t row_bytes = (size_t)s->M * (sizeof(double) + sizeof(uint32_t));
+  int hist_cap = (int)std::min<size_t>(std::min<size_t>(max_pairs, 512), (48 * 1024) / row_bytes);
+  hist_cap &= ~1;  // keeps the records after the ratio rows 16-byte aligned
+  room -= (size_t)hist_cap * row_bytes;
+  const int cand_cap = (int)std::min<size_t>(max_pairs, room / (sizeof(Cand) + 4) & ~(size_t)3);
+  hist_cap = std::min(hist_cap, cand_cap & ~1);
+  const size_t dyn = fixed + (size_t)hist_cap * row_bytes + (size_t)cand_cap * (sizeof(Cand) + 4);
   const size_t g_over = max_pairs > (size_t)cand_cap ? max_pairs - cand_cap : 1;
-  const size_t g_det = max_pairs > (size_t)det_cap ? max_pairs - det_cap : 1;
-  if ((rc = s->d_cpos.ensure(g_over * 4)) || (rc = s->d_cmask.ensure(g_over * 4)) ||
-      (rc = s->d_det.ensure(g_det * sizeof(Det))) ||
+  if ((rc = s->d_cpos.ensure(g_over * 4)) || (rc = s->d_det.ensure(g_over * sizeof(Cand))) ||
       (rc = s->d_nodes.ensure((size_t)std::max(1, max_nodes - kSmemNodes) * sizeof(Node))))
     return rc;
   if (!s->attr_set) {
@@ -1310,49 +1589,53 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.N = s->N;
   A.M = s->M;
   A.B = B;
-  A.order = (const int32_t*)s->d_order.p;
-  A.cidx = cidx_host ? (const int32_t*)((char*)s->d_upd.p + off_cidx) : nullptr;
   A.Q = Q;
+  A.npairs = s->npairs;
+  A.order = (int32_t*)s->d_order.p;
+  A.cidx = cidx_host ? (int32_t*)s->d_cidx.p : nullptr;
   A.ready = (uint64_t*)s->d_ready.p;
-  A.n_upd = (int)nu;
-  A.upd_mask = (const uint64_t*)s->d_upd.p;
-  A.upd_slot = (const int32_t*)((char*)s->d_upd.p + nu * 8);
   A.cand = (const uint32_t*)s->d_cand.p;
   A.hist = (const uint32_t*)s->d_hist.p;
-  A.nviable = (const uint32_t*)s->d_nv.p;
   A.voff = (const uint64_t*)s->d_voff.p;
   A.pool = (const uint32_t*)s->d_pool.p;
+  A.nviable = (const uint32_t*)s->d_nv.p;
   A.ids = (const uint64_t*)s->d_ids.p;
+  A.ever = (const uint32_t*)((char*)s->d_status.p + 8);
+  A.h_upd_mask = (const uint64_t*)hd;
+  A.h_upd_slot = (const int32_t*)(hd + off_slot);
+  A.n_upd = (int)nu;
+  A.h_tail = (const int32_t*)(hd + off_tail);
+  A.tail_from = (int)tail_from;
+  A.n_tail = (int)n_tail;
+  A.h_cidx = cidx_host ? (const int32_t*)(hd + off_cidx) : nullptr;
   std::memcpy(A.prio, s->prio, sizeof A.prio);
   for (int t = 0; t < s->N; ++t) A.prio_rank[(int)s->prio[t]] = (int8_t)t;
   std::memcpy(A.place, s->place, sizeof A.place);
   std::memcpy(A.place_magic, s->place_magic, sizeof A.place_magic);
   A.div_m = ctx->space->dev().div_m;
   A.eng = ed;
-  A.gcpos = (uint32_t*)s->d_cpos.p;
-  A.gcmask = (uint32_t*)s->d_cmask.p;
-  A.gdet = (Det*)s->d_det.p;
+  A.gmask = (uint32_t*)s->d_cpos.p;
+  A.grec = (Cand*)s->d_det.p;
   A.cand_cap = cand_cap;
-  A.det_cap = det_cap;
   A.hist_cap = hist_cap;
   A.gnodes = (Node*)s->d_nodes.p;
   A.max_nodes = max_nodes;
   A.max_children = max_children;
-  A.out = (int32_t*)s->d_out.p;
+  A.out = out_d;
   A.triples_cap = cap_t;
   A.timing = (unsigned long long*)((char*)s->d_status.p + 32);
   A.async_status = (int32_t*)s->d_status.p;
   {
     Launch L(ctx, K_SCHED_ROUND);
-    k_sched_round<<<1, kRoundThreads, dyn, st>>>(A);
+    k_sched_round<<<1, kRoundThreads, dyn, ctx->stream>>>(A);
   }
   AG_CUDA(cudaGetLastError());
-  char* hr = (char*)s->h_res;
-  AG_CUDA(cudaMemcpyAsync(hr, s->d_out.p, res_bytes, cudaMemcpyDeviceToHost, st));
-  AG_CUDA(cudaStreamSynchronize(st));
+  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  s->dirty_from = Q;
   s->upd_slot.clear();
   s->upd_mask.clear();
-  const int32_t status = ((int32_t*)hr)[0];
+  const char* hr = (const char*)s->h_res;
+  const int32_t status = ((const int32_t*)hr)[0];
   if (status) {
     if (status == AG_ERR_VALIDATION + 100)
       return fail(AG_ERR_VALIDATION, "viable model tier without an engine pool");
@@ -1401,6 +1684,7 @@ int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_
   if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N <= 2^32 and N <= 32");
   if (sp->m > 32) return fail(AG_ERR_VALIDATION, "GPU scheduler supports at most 32 model tiers");
   if (max_requests < 1) return fail(AG_ERR_VALIDATION, "max_requests < 1");
+  if (max_requests >= (1 << 26)) return fail(AG_ERR_VALIDATION, "GPU scheduler supports < 2^26 requests per session");
   ag_sched* s = new ag_sched();
   s->ctx = ctx;
   s->N = sp->n;
@@ -1476,14 +1760,12 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
       s->stages[(size_t)slot * N + a] =
           q->stages ? q->stages[(size_t)i * N + a]
                     : (ctx->space->pred[a] ? AG_STAGE_PENDING : AG_STAGE_READY);
-    s->ready[slot] = agb::ready_of(s, slot);
     s->live[slot] = 1;
     s->nviable[slot] = (uint32_t)(q->viable_ptr[i + 1] - q->viable_ptr[i]);
     meta[3 * i] = s->pool_top + (uint64_t)(q->viable_ptr[i] - q->viable_ptr[0]);
     meta[3 * i + 1] = s->nviable[slot];
     meta[3 * i + 2] = q->ids[i];
-    s->upd_slot.push_back(slot);
-    s->upd_mask.push_back(s->ready[slot]);
+    agb::set_ready(s, slot, agb::ready_of(s, slot));
     if (slots_out) slots_out[i] = slot;
   }
   AG_CUDA(cudaMemcpyAsync((uint32_t*)s->d_pool.p + s->pool_top, q->viable + q->viable_ptr[0],
@@ -1506,7 +1788,8 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
     s->dirty_from = std::min(s->dirty_from, pos);
   }
   // the viable copy must land before the histogram pass reads it (same stream)
-  return agb::launch_prune(s, slots, g_begin, {}, &meta);
+  const int rc = agb::launch_prune(s, slots, g_begin, {}, &meta);
+  return rc ? rc : agb::flush_order(s);
 }
 
 int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
@@ -1515,9 +1798,7 @@ int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
     const int slot = slots[i];
     if (slot < 0 || slot >= s->cap || !s->live[slot]) return fail(AG_ERR_VALIDATION, "bad slot");
     s->live[slot] = 0;
-    s->ready[slot] = 0;
-    s->upd_slot.push_back(slot);
-    s->upd_mask.push_back(0);
+    agb::set_ready(s, slot, 0);
     s->quarantine.push_back(slot);  // still listed on the device until compaction
     ++s->dead;
   }
@@ -1528,7 +1809,7 @@ int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
     agb::compact_order(s);
     s->pool_top = 0;  // everything left: reuse the pool
   }
-  return AG_OK;
+  return agb::flush_order(s);
 }
 
 int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent) {
@@ -1548,11 +1829,7 @@ int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent) {
     if (all_done) st[sc] = AG_STAGE_READY;
   }
   const uint64_t r = agb::ready_of(s, slot);
-  if (r != s->ready[slot]) {
-    s->ready[slot] = r;
-    s->upd_slot.push_back(slot);
-    s->upd_mask.push_back(r);
-  }
+  if (r != s->ready[slot]) agb::set_ready(s, slot, r);
   return AG_OK;
 }
 
@@ -1589,10 +1866,7 @@ int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
   }
   g_begin.push_back((int32_t)g_am.size());
   for (int slot : g_slot) {
-    const uint64_t r = agb::ready_of(s, slot);
-    s->ready[slot] = r;
-    s->upd_slot.push_back(slot);
-    s->upd_mask.push_back(r);
+    agb::set_ready(s, slot, agb::ready_of(s, slot));
   }
   return agb::launch_prune(s, g_slot, g_begin, g_am, nullptr);
 }
@@ -1633,7 +1907,7 @@ int ag_sched_queued_ahead(ag_sched* s, int32_t* out) {
 
 int ag_sched_round_timing(ag_sched* s, uint64_t* ns) {
   if (!s || !ns) return fail(AG_ERR_VALIDATION, "null argument");
-  AG_CUDA(cudaMemcpyAsync(ns, (char*)s->d_status.p + 32, 104, cudaMemcpyDeviceToHost, s->ctx->stream));
+  AG_CUDA(cudaMemcpyAsync(ns, (char*)s->d_status.p + 32, 128, cudaMemcpyDeviceToHost, s->ctx->stream));
   AG_CUDA(cudaStreamSynchronize(s->ctx->stream));
   return AG_OK;
 }

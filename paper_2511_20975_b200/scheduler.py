@@ -153,12 +153,16 @@ class SchedSession:
         check(lib().ag_sched_dispatch(self._h, len(idx), arr))
 
     def round_timing(self):
-        """Device phase durations (us) of the last round: context, candidates,
-        walk, finalize."""
-        t = np.zeros(13, np.uint64)
+        """Device phase durations (us) of the last round: setup, first
+        candidate chunk, walk, finalize.  Also sets walk_cycles (find, build,
+        rank, adopt), walk_counts (steps, children) and chunk_us (the first
+        producer chunk: loads, scan, records, histogram rows)."""
+        t = np.zeros(16, np.uint64)
         check(lib().ag_sched_round_timing(self._h, C.c_void_p(_ptr(t))))
         self.walk_cycles = t[5:9].astype(np.float64)
-        self.ctx_cycles = t[9:13].astype(np.float64)
+        self.walk_counts = t[9:11].astype(np.int64)
+        self.ctx_cycles = self.walk_counts
+        self.chunk_us = np.diff(np.concatenate([[float(t[1])], t[11:15].astype(np.float64)])) / 1e3
         return np.diff(t[:5].astype(np.float64)) / 1e3
 
     def last_round_us(self) -> float:
