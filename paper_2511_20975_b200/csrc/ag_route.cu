@@ -28,6 +28,7 @@
 //             the noise can change are hashed.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -377,13 +378,12 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
     const uint32_t o = it * 32u + lane;  // word wbeg + o, owned by lane it
     if (o < nw) brow[o] = s_tr[wid][it][lane];
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if (lane == 0) a.task_counts[task] = cnt;
+  // per-group counts (group = the 32 words of one lane) for the compaction
+  a.task_counts[(size_t)task * 32 + lane] = cnt;
 }
 
-// K2a: one warp per request: exclusive scan of its task counts -> task
-// offsets (relative to the request), counts[r] = request total.
+// K2a: one warp per request: exclusive scan of its group counts (32 per
+// warp-task) -> group offsets relative to the request, counts[r] = total.
 __global__ void __launch_bounds__(kThreads)
     k_chunk_scan(const uint32_t* __restrict__ task_counts, uint64_t* __restrict__ task_off,
                  uint64_t* __restrict__ counts, uint32_t C, int R) {
@@ -408,17 +408,67 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0) counts[r] = carry;
 }
 
+// K2a for long requests (deep spaces): one block per request; each thread
+// sums a contiguous run, a block scan gives the run offsets, then the runs
+// are written.
+__global__ void __launch_bounds__(1024)
+    k_chunk_scan_block(const uint32_t* __restrict__ task_counts, uint64_t* __restrict__ task_off,
+                       uint64_t* __restrict__ counts, uint32_t C) {
+  __shared__ uint64_t warp_sums[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int r = blockIdx.x;
+  const uint32_t* in = task_counts + (size_t)r * C;
+  uint64_t* out = task_off + (size_t)r * C;
+  const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(C, threadIdx.x * per), hi = min(C, lo + per);
+  uint64_t local = 0;
+  for (uint32_t i = lo; i < hi; ++i) local += in[i];
+  uint64_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const uint64_t v = lane < (int)(blockDim.x / 32) ? warp_sums[lane] : 0;
+    uint64_t z = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < (int)(blockDim.x / 32)) warp_sums[lane] = z - v;
+    if (lane == 31) counts[r] = z;
+  }
+  __syncthreads();
+  uint64_t run = warp_sums[wid] + x - local;
+  for (uint32_t i = lo; i < hi; ++i) {
+    out[i] = run;
+    run += in[i];
+  }
+}
+
 // K2b: exclusive scan over requests -> offsets[R+1], overflow flag.  One
-// block; each thread owns a contiguous run of requests.
+// block; each thread owns a contiguous run of requests, read and written in
+// register batches so the loads of a run are in flight together.
 __global__ void __launch_bounds__(1024)
     k_request_scan(const uint64_t* __restrict__ counts, uint64_t* __restrict__ offsets, int R,
                    uint64_t capacity, uint32_t* __restrict__ overflow) {
+  constexpr int kB = 8;
   __shared__ uint64_t warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int per = (R + 1023) / 1024;
   const int lo = min(R, (int)threadIdx.x * per), hi = min(R, lo + per);
   uint64_t local = 0;
-  for (int i = lo; i < hi; ++i) local += counts[i];
+  for (int i0 = lo; i0 < hi; i0 += kB) {
+    uint64_t v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
+#pragma unroll
+    for (int u = 0; u < kB; ++u) local += v[u];
+  }
   uint64_t x = local;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -438,9 +488,16 @@ __global__ void __launch_bounds__(1024)
   }
   __syncthreads();
   uint64_t run = warp_sums[wid] + x - local;
-  for (int i = lo; i < hi; ++i) {
-    offsets[i] = run;
-    run += counts[i];
+  for (int i0 = lo; i0 < hi; i0 += kB) {
+    uint64_t v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
+#pragma unroll
+    for (int u = 0; u < kB; ++u)
+      if (i0 + u < hi) {
+        offsets[i0 + u] = run;
+        run += v[u];
+      }
   }
   if (hi == R && lo < hi) {
     offsets[R] = run;
@@ -449,70 +506,102 @@ __global__ void __launch_bounds__(1024)
 }
 
 // K3: stream compaction of the verdict bitmap into canonical-order indices.
-// Each iteration the warp loads 32 words (coalesced), scans their popcounts,
-// then walks the non-empty words: the 32 lanes test the 32 bits and the set
-// lanes store their index at prefix(word) + popc(word & lanemask_lt) -- one
-// contiguous run per store instruction, no shared memory.
+// Work unit = kUnitGroups groups of 32 words (each group's output offset is
+// known from K2a); persistent warps stride over units.  Per iteration the warp
+// loads 32 words (coalesced, software-pipelined) and scans their popcounts;
+// the members are staged bit-parallel in shared memory -- for word w lane j
+// stores member (w, j) at prefix(w) + popc(word_w & lanemask_lt), a
+// conflict-free contiguous run, with words / prefixes read four at a time by
+// broadcast 16-byte loads -- aligned to the output's 16-byte phase, and every
+// full 16-byte vector is written back at once; the <= 3 trailing members carry
+// over to the next iteration, so global stores are almost all full vectors.
+constexpr int kStage = 32 * 32 + 8;  // one iteration's members + carry + pad
+constexpr uint32_t kUnitGroups = 8;
+
 __global__ void __launch_bounds__(kThreads)
-    k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ task_off,
+    k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ group_off,
                     const uint64_t* __restrict__ offsets, uint64_t begin, uint32_t W, uint32_t C,
-                    uint64_t div_c, int R, uint32_t* __restrict__ indices, uint64_t capacity) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t task = blockIdx.x * kWarpsPerBlock + (threadIdx.x >> 5);
-  if ((uint64_t)task >= (uint64_t)R * C) return;
-  const uint32_t r = C == 1 ? task : (uint32_t)__umul64hi(task, div_c);
-  const uint32_t c = task - r * C;
-  uint64_t base = __ldg(offsets + r) + __ldg(task_off + task);
-  const uint32_t lt = (1u << lane) - 1u;
-  const uint32_t* brow = bitmap + (size_t)r * W;
-  const uint32_t wbeg = c * kTaskWords;
-  const uint32_t wend = min(W, wbeg + kTaskWords);
-  uint32_t next = wbeg + lane < wend ? __ldg(brow + wbeg + lane) : 0u;
-  for (uint32_t wb = wbeg; wb < wend; wb += 32) {
-    const uint32_t word = next;  // software-pipelined: fetch the next 32 words now
-    const uint32_t wn = wb + 32 + lane;
-    next = wn < wend ? __ldg(brow + wn) : 0u;
-    uint32_t nz = __ballot_sync(0xffffffffu, word != 0);
-    if (!nz) continue;
-    const uint32_t pc = __popc(word);
-    uint32_t x = pc;
+                    uint32_t units_per_req, uint64_t div_u, int R, uint32_t* __restrict__ indices,
+                    uint64_t capacity) {
+  __shared__ __align__(16) uint32_t s_stage[kWarpsPerBlock][kStage];
+  __shared__ __align__(16) uint32_t s_word[kWarpsPerBlock][32];
+  __shared__ __align__(16) uint32_t s_pre[kWarpsPerBlock][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u, bit = 1u << lane;
+  uint32_t* st = s_stage[wid];
+  const uint64_t units = (uint64_t)R * units_per_req;
+  const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
+  for (uint64_t unit = (uint64_t)blockIdx.x * kWarpsPerBlock + wid; unit < units; unit += nwarps) {
+    const uint32_t r = units_per_req == 1 ? (uint32_t)unit : (uint32_t)__umul64hi(unit, div_u);
+    const uint32_t u = (uint32_t)unit - r * units_per_req;
+    const uint32_t g0 = u * kUnitGroups;  // first group (32 words each)
+    const uint32_t wbeg = g0 * 32;
+    const uint32_t wend = min(W, wbeg + 32 * kUnitGroups);
+    // global output position of the unit's first member
+    const uint64_t gs = __ldg(offsets + r) + __ldg(group_off + (size_t)r * C * 32 + g0);
+    const uint32_t* brow = bitmap + (size_t)r * W;
+    const uint32_t phase0 = (uint32_t)(reinterpret_cast<uintptr_t>(indices + gs) >> 2) & 3u;
+    uint32_t* gal = indices + (gs - phase0);  // 16-byte aligned output cursor (stage[0])
+    uint64_t gpos = gs - phase0;              // its global index
+    uint32_t fill = phase0;  // stage[0, fill): carried members (or, at first, not ours)
+    uint32_t skip = phase0;  // leading stage entries that are not ours (first vector only)
+    uint32_t next = wbeg + lane < wend ? __ldg(brow + wbeg + lane) : 0u;
+    for (uint32_t wb = wbeg; wb < wend; wb += 32) {
+      const uint32_t word = next;
+      const uint32_t wn = wb + 32 + lane;
+      next = wn < wend ? __ldg(brow + wn) : 0u;
+      const uint32_t pc = __popc(word);
+      uint32_t x = pc;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
-    }
-    const uint32_t excl = x - pc;
-    const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
-    const uint32_t ibase = (uint32_t)(begin + (uint64_t)wb * 32) + (uint32_t)lane;
-    const uint64_t out = (uint64_t)(indices + base);
-    if (base + total <= capacity) {
-      const uint32_t bit = 1u << lane;
-      while (nz) {
-        // any order works: every word owns a precomputed output range
-        const int src = 31 - __clz(nz);
-        nz ^= 1u << src;
-        const uint32_t ww = __shfl_sync(0xffffffffu, word, src);
-        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
-        const uint32_t rank = pre + __popc(ww & lt);
-        const uint32_t val = ibase + ((uint32_t)src << 5);
-        // predicated store at out + 4*rank (one wide mad), no branch
-        asm volatile(
-            "{ .reg .pred p; .reg .u64 a; setp.ne.u32 p, %3, 0;"
-            " mad.wide.u32 a, %1, 4, %0; @p st.global.u32 [a], %2; }" ::"l"(out),
-            "r"(rank), "r"(val), "r"(ww & bit)
-            : "memory");
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
       }
-    } else {
-      while (nz) {
-        const int src = __ffs(nz) - 1;
-        nz &= nz - 1;
-        const uint32_t ww = __shfl_sync(0xffffffffu, word, src);
-        const uint32_t pre = __shfl_sync(0xffffffffu, excl, src);
-        const uint64_t o = base + pre + __popc(ww & lt);
-        if (((ww >> lane) & 1u) && o < capacity) indices[o] = ibase + (uint32_t)src * 32u;
+      const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
+      if (total == 0) continue;
+      s_word[wid][lane] = word;
+      s_pre[wid][lane] = x - pc + fill;
+      __syncwarp();
+      const uint32_t vl = (uint32_t)(begin + (uint64_t)wb * 32) + (uint32_t)lane;
+#pragma unroll
+      for (int w4 = 0; w4 < 32; w4 += 4) {
+        const uint4 ww = *reinterpret_cast<const uint4*>(&s_word[wid][w4]);
+        const uint4 pp = *reinterpret_cast<const uint4*>(&s_pre[wid][w4]);
+        if (ww.x & bit) st[pp.x + __popc(ww.x & lt)] = vl + 32u * (w4 + 0);
+        if (ww.y & bit) st[pp.y + __popc(ww.y & lt)] = vl + 32u * (w4 + 1);
+        if (ww.z & bit) st[pp.z + __popc(ww.z & lt)] = vl + 32u * (w4 + 2);
+        if (ww.w & bit) st[pp.w + __popc(ww.w & lt)] = vl + 32u * (w4 + 3);
       }
+      __syncwarp();
+      // full vectors now; the partial last vector carries over
+      const uint32_t end = fill + total;
+      const uint32_t nfull = end >> 2;
+      const bool in_cap = gpos + 4ull * nfull <= capacity;
+      for (uint32_t v = lane; v < nfull; v += 32) {
+        const uint32_t e0 = 4 * v;
+        if (e0 >= skip && in_cap) {
+          *reinterpret_cast<uint4*>(gal + e0) = *reinterpret_cast<const uint4*>(st + e0);
+        } else {
+#pragma unroll
+          for (uint32_t q = 0; q < 4; ++q) {
+            const uint32_t e = e0 + q;
+            if (e >= skip && gpos + e < capacity) gal[e] = st[e];
+          }
+        }
+      }
+      const uint32_t tail = end & 3u;
+      const uint32_t t0 = lane < tail ? st[4 * nfull + lane] : 0u;
+      __syncwarp();
+      if (lane < tail) st[lane] = t0;
+      if (nfull) skip = 0;
+      fill = tail;
+      gal += 4 * nfull;
+      gpos += 4ull * nfull;
+      __syncwarp();
     }
-    base += total;
+    // the last partial vector
+    if (lane >= skip && lane < fill && gpos + lane < capacity) gal[lane] = st[lane];
+    __syncwarp();
   }
 }
 
@@ -586,6 +675,31 @@ int make_router(const ag_router* r, RouterDev* out) {
   return AG_OK;
 }
 
+// K3 launch: persistent warps over units of kUnitGroups groups, the grid
+// sized to the device's resident capacity for this kernel.
+int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, const uint32_t* bitmap,
+                   const uint64_t* offsets, uint32_t* indices, uint64_t capacity) {
+  static int resident = 0;  // blocks per device (SMs x blocks per SM)
+  if (!resident) {
+    int dev = 0, sms = 0, per_sm = 0;
+    AG_CUDA(cudaGetDevice(&dev));
+    AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_route_compact, kThreads, 0));
+    resident = std::max(1, sms * per_sm);
+  }
+  const uint32_t ngroups = (W + 31) / 32;
+  const uint32_t upr = (ngroups + kUnitGroups - 1) / kUnitGroups;
+  const uint64_t units = (uint64_t)R * upr;
+  if (units >= (1ULL << 32)) return fail(AG_ERR_VALIDATION, "batch too large for one launch");
+  const uint64_t want = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)resident));
+  Launch L(ctx, K_ROUTE_COMPACT);
+  k_route_compact<<<blocks, kThreads, 0, ctx->stream>>>(bitmap, (const uint64_t*)ctx->chunk_off.p, offsets,
+                                                        begin, W, C, upr, magic_div(upr), R, indices, capacity);
+  AG_CUDA(cudaGetLastError());
+  return AG_OK;
+}
+
 int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t begin,
                     uint64_t end, uint32_t flags, const ag_route_out* out) {
   const ag_space* sp = ctx->space;
@@ -610,8 +724,8 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   const uint64_t ntasks = (uint64_t)R * C;
   if (ntasks >= (1ULL << 31)) return fail(AG_ERR_VALIDATION, "batch too large for one launch");
 
-  if ((rc = ctx->chunk_counts.ensure(ntasks * 4))) return rc;
-  if ((rc = ctx->chunk_off.ensure(ntasks * 8))) return rc;
+  if ((rc = ctx->chunk_counts.ensure(ntasks * 32 * 4))) return rc;
+  if ((rc = ctx->chunk_off.ensure(ntasks * 32 * 8))) return rc;
   if ((rc = ensure_colmask(ctx))) return rc;
   uint32_t* bitmap = out->bitmap;
   if (!bitmap) {
@@ -648,8 +762,12 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
     }
     {
       Launch L(ctx, K_CHUNK_SCAN);
-      k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
-          (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C, R);
+      if (C * 32 <= 4096)
+        k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
+            (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
+      else
+        k_chunk_scan_block<<<R, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
+                                              (uint64_t*)ctx->chunk_off.p, out->counts, C * 32);
     }
   } else {
     AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
@@ -660,16 +778,14 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
                                      out->indices ? out->capacity : ~0ULL, out->overflow);
   }
   if (out->indices && range > 0) {
-    Launch L(ctx, K_ROUTE_COMPACT);
-    k_route_compact<<<grid, kThreads, 0, s>>>(bitmap, (const uint64_t*)ctx->chunk_off.p, offsets,
-                                              begin, W, C, magic_div(C), R, out->indices,
-                                              out->capacity);
+    rc = launch_compact(ctx, R, W, C, begin, bitmap, offsets, out->indices, out->capacity);
+    if (rc) return rc;
   }
   AG_CUDA(cudaGetLastError());
   return AG_OK;
 }
 
-// Compaction pass alone, reusing the task offsets of the preceding
+// Compaction pass alone, reusing the group offsets of the preceding
 // route_enumerate on this context (the host path's second phase).
 int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32_t* bitmap,
                   const uint64_t* offsets, uint32_t* indices, uint64_t capacity) {
@@ -677,14 +793,7 @@ int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32
   if (R == 0 || range == 0) return AG_OK;
   const uint32_t W = (uint32_t)((range + 31) / 32);
   const uint32_t C = (W + kTaskWords - 1) / kTaskWords;
-  const uint64_t ntasks = (uint64_t)R * C;
-  const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
-  Launch L(ctx, K_ROUTE_COMPACT);
-  k_route_compact<<<grid, kThreads, 0, ctx->stream>>>(bitmap, (const uint64_t*)ctx->chunk_off.p,
-                                                      offsets, begin, W, C, magic_div(C), R,
-                                                      indices, capacity);
-  AG_CUDA(cudaGetLastError());
-  return AG_OK;
+  return launch_compact(ctx, R, W, C, begin, bitmap, offsets, indices, capacity);
 }
 
 }  // namespace agb

@@ -21,3 +21,20 @@ tot = sum(agg.values())
 print("samples", tot)
 for k, s in agg.most_common(top):
     print(f"{s:6d} {100*s/tot:5.1f}% {k[0]}:{k[1]}  {text.get(k,'')}")
+
+# per-line stall breakdown for the top lines (set NCU_STALLS=1)
+import os
+if os.environ.get("NCU_STALLS"):
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    per = collections.defaultdict(collections.Counter)
+    cur = None
+    for r in rows:
+        if len(r) == 2 and r[0] == "File Path":
+            fname = r[1].split("/")[-1]; continue
+        if not r or r[0] == "Line No" or len(r) < len(hdr): continue
+        if r[0].strip(): cur = (fname, int(r[0]))
+        for i in cols:
+            try: per[cur][hdr[i]] += int(r[i])
+            except ValueError: pass
+    for k, s in agg.most_common(min(top, 8)):
+        print(k, per[k].most_common(4))
