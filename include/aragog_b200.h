@@ -194,6 +194,17 @@ int ag_predict(ag_predictor* p, const ag_truth* truth_dev,
                const ag_router* router, const double* budgets,
                double budget_all, const ag_predict_out* out_dev);
 
+/* ag_predict with host buffers, copies included (the path a drop-in
+ * ConfigPredictor::predict takes): truth and budgets [R] host; viable
+ * [R * viable_stride], n_viable [R] required; search_evals, verify_evals,
+ * router_time, truncated [R] optional. */
+int ag_predict_host(ag_predictor* p, const ag_truth* truth_host,
+                    const ag_router* router, const double* budgets,
+                    double budget_all, uint32_t* viable, int32_t viable_stride,
+                    int32_t* n_viable, int32_t* search_evals,
+                    int32_t* verify_evals, double* router_time,
+                    uint8_t* truncated);
+
 /* ======================================================================== *
  * Per-stage scheduling (hot path 2)                                         *
  * ======================================================================== */
@@ -315,6 +326,15 @@ int ag_select_per_input(ag_ctx* ctx, const uint32_t* members,
                         const uint64_t* offsets, int32_t n_requests,
                         int32_t kind, const ag_load* load, uint32_t* chosen,
                         double* est);
+
+/* select_per_input_config(accurate, space, kind, load) (workload.cpp:149-176)
+ * for a batch of host AccurateSets, end to end on the device: every set's
+ * members are enumerated (enumerate_members, accuracy.cpp:227-238, without its
+ * 4096-config guard) and compacted, then re-costed and arg-minned as
+ * ag_select_per_input.  chosen [R] host canonical indices, est [R] optional. */
+int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* truth_host,
+                             int32_t kind, const ag_load* load,
+                             uint32_t* chosen, double* est);
 
 /* snapshot_load's queued_ahead (simulation.cpp:194-213): per model tier, the
  * number of ready (request, agent) pairs of the session whose candidate set

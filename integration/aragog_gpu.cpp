@@ -1,0 +1,406 @@
+// Drop-in adapter: the reference's hot-path symbols implemented over the C ABI
+// of libaragog_b200.so (include/aragog_b200.h), compiled against the
+// reference headers (/root/reference/proj/include) so the reference
+// simulator, metrics and acceptance criteria relink unchanged
+// (SURVEY.md §8(b) "Adapter TU", §8(f) rank 1).
+//
+//   ConfigPredictor::predict      (src/predictor.cpp:165-262) -> ag_predict_host
+//   beam_schedule                 (src/scheduler.cpp:289-378) -> ag_beam_schedule
+//   enumerate_members             (src/accuracy.cpp:227-238)  -> ag_route_enumerate_host
+//   select_per_input_config       (src/workload.cpp:149-176)  -> ag_select_per_input_host
+//
+// The reference objects are linked with these four symbols weakened
+// (objcopy --weaken-symbol, integration/Makefile), so the definitions below
+// win at link time.  There is no CPU fallback: a RouterBackend that is not an
+// OracleRouter (or a NoisyRouter over one) -- e.g. the CountingRouter test
+// decorator (tests/predictor_test.cpp:52-67) -- is rejected with a
+// ValidationError, as is anything outside the GPU path's limits.
+//
+// Threading: predictions may run concurrently; every GPU call
+// here is serialised by one mutex, contexts are cached per distinct space.
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "aragog/accuracy.h"
+#include "aragog/engine.h"
+#include "aragog/errors.h"
+#include "aragog/predictor.h"
+#include "aragog/request.h"
+#include "aragog/router.h"
+#include "aragog/scheduler.h"
+#include "aragog/workload.h"
+#include "aragog_b200.h"
+
+namespace {
+
+// ---- private-member access: an explicit instantiation may name private
+// members; the friend function hands the member pointer out.
+template <class Tag, typename Tag::type M>
+struct Rob {
+  friend typename Tag::type get(Tag) { return M; }
+};
+struct OracleTable {
+  using type = const aragog::AccuracyTable* aragog::OracleRouter::*;
+  friend type get(OracleTable);
+};
+template struct Rob<OracleTable, &aragog::OracleRouter::table_>;
+struct NoisyInner {
+  using type = const aragog::RouterBackend* aragog::NoisyRouter::*;
+  friend type get(NoisyInner);
+};
+template struct Rob<NoisyInner, &aragog::NoisyRouter::inner_>;
+struct NoisyFp {
+  using type = double aragog::NoisyRouter::*;
+  friend type get(NoisyFp);
+};
+template struct Rob<NoisyFp, &aragog::NoisyRouter::fp_>;
+struct NoisyFn {
+  using type = double aragog::NoisyRouter::*;
+  friend type get(NoisyFn);
+};
+template struct Rob<NoisyFn, &aragog::NoisyRouter::fn_>;
+struct NoisySeed {
+  using type = std::uint64_t aragog::NoisyRouter::*;
+  friend type get(NoisySeed);
+};
+template struct Rob<NoisySeed, &aragog::NoisyRouter::seed_>;
+struct PredRouter {
+  using type = const aragog::RouterBackend* aragog::ConfigPredictor::*;
+  friend type get(PredRouter);
+};
+template struct Rob<PredRouter, &aragog::ConfigPredictor::router_>;
+
+// errors.h:22-34 taxonomy from the C ABI status
+void check(int rc) {
+  if (rc == AG_OK) return;
+  const std::string msg = ag_last_error();
+  if (rc == AG_ERR_VALIDATION) throw aragog::ValidationError(msg);
+  if (rc == AG_ERR_IO) throw aragog::IoError(msg);
+  throw std::logic_error("aragog_b200: " + msg);
+}
+
+std::mutex g_mu;
+
+// One GPU space + context per distinct (graph, catalog); predictors per plan.
+struct Gpu {
+  ag_space* space = nullptr;
+  ag_ctx* ctx = nullptr;
+  int n = 0, m = 0;
+  std::uint64_t size = 0;
+  std::map<std::pair<int, int>, ag_predictor*> preds;  // (chains, exhaustive)
+  int viable_cap = 0;
+};
+
+std::map<std::string, std::unique_ptr<Gpu>>& cache() {
+  static std::map<std::string, std::unique_ptr<Gpu>> c;
+  return c;
+}
+
+template <class T>
+void put(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof v);
+}
+
+// Space for a graph with M tiers of the given costs / slot throughputs.
+Gpu& gpu_for(const aragog::WorkflowGraph& g, const std::vector<double>& cost,
+             const std::vector<double>& thr) {
+  const int n = g.num_agents(), m = (int)cost.size();
+  std::string key;
+  put(key, n);
+  put(key, m);
+  std::vector<int32_t> edges;  // (from, to) by declaration index
+  for (int p = 0; p < n; ++p) {
+    put(key, g.declaration_index(p));
+    for (int q : g.successors(p)) {
+      edges.push_back(g.declaration_index(p));
+      edges.push_back(g.declaration_index(q));
+    }
+  }
+  for (int32_t e : edges) put(key, e);
+  for (double c : cost) put(key, c);
+  for (double t : thr) put(key, t);
+  auto& c = cache();
+  auto it = c.find(key);
+  if (it != c.end()) return *it->second;
+  auto gp = std::make_unique<Gpu>();
+  check(ag_space_create(n, (int)edges.size() / 2, edges.data(), m, cost.data(), thr.data(),
+                        &gp->space));
+  int32_t nn = 0, mm = 0;
+  std::vector<int32_t> decl(n), depth(n);
+  check(ag_space_info(gp->space, &nn, &mm, decl.data(), depth.data(), &gp->size));
+  for (int p = 0; p < n; ++p)
+    if (decl[p] != g.declaration_index(p) || depth[p] != g.depth(p))
+      throw std::logic_error("aragog_b200: canonical agent order differs from WorkflowGraph");
+  check(ag_ctx_create(gp->space, 0, &gp->ctx));
+  gp->n = n;
+  gp->m = m;
+  Gpu& ref = *gp;
+  c.emplace(key, std::move(gp));
+  return ref;
+}
+
+Gpu& gpu_for(const aragog::ConfigSpace& s) {
+  std::vector<double> cost, thr;
+  for (const aragog::ModelSpec& ms : s.catalog().models()) {
+    cost.push_back(ms.cost);
+    thr.push_back(ms.slot_throughput);
+  }
+  return gpu_for(s.graph(), cost, thr);
+}
+
+std::uint64_t index_of(const std::vector<int>& models, int m) {
+  std::uint64_t x = 0;
+  for (int d : models) x = x * (std::uint64_t)m + (std::uint64_t)d;
+  return x;
+}
+
+// AccurateSet (accuracy.h:34-40) as a one-request ag_truth batch
+struct Truth {
+  std::uint64_t id;
+  int32_t seed_ptr[2], removed_ptr[2];
+  std::vector<uint8_t> seeds;
+  std::vector<std::uint64_t> removed;
+  ag_truth c;
+  Truth(const aragog::AccurateSet& set, aragog::RequestId rid, int n, int m) : id(rid) {
+    for (const aragog::Configuration& s : set.seeds) {
+      if ((int)s.models.size() != n) throw aragog::ValidationError("configuration length mismatch");
+      for (int d : s.models) seeds.push_back((uint8_t)d);
+    }
+    for (const aragog::Configuration& r : set.removed) removed.push_back(index_of(r.models, m));
+    seed_ptr[0] = 0;
+    seed_ptr[1] = (int32_t)set.seeds.size();
+    removed_ptr[0] = 0;
+    removed_ptr[1] = (int32_t)removed.size();
+    c = ag_truth{1, &id, seed_ptr, seeds.data(), removed_ptr, removed.data()};
+  }
+};
+
+// RouterBackend -> ag_router + the table it reads (no CPU fallback)
+struct RouterView {
+  ag_router r{};
+  const aragog::AccuracyTable* table = nullptr;
+};
+
+RouterView router_view(const aragog::RouterBackend* rb) {
+  RouterView v;
+  if (auto* o = dynamic_cast<const aragog::OracleRouter*>(rb)) {
+    v.r = ag_router{AG_ROUTER_ORACLE, 0.0, 0.0, 0, o->eval_latency()};
+    v.table = o->*get(OracleTable());
+    return v;
+  }
+  if (auto* nz = dynamic_cast<const aragog::NoisyRouter*>(rb)) {
+    auto* inner = dynamic_cast<const aragog::OracleRouter*>(nz->*get(NoisyInner()));
+    if (inner) {
+      v.r = ag_router{AG_ROUTER_NOISY, nz->*get(NoisyFp()), nz->*get(NoisyFn()), nz->*get(NoisySeed()),
+                      nz->eval_latency()};
+      v.table = inner->*get(OracleTable());
+      return v;
+    }
+  }
+  throw aragog::ValidationError(
+      "GPU predictor supports OracleRouter and NoisyRouter over an OracleRouter only");
+}
+
+// GPU predictor reproducing the reference plan (checked once, chain by chain)
+ag_predictor* predictor_for(Gpu& g, const aragog::ConfigSpace& space, const aragog::ChainPlan& plan) {
+  const std::pair<int, int> key{(int)plan.chains.size(), plan.exhaustive ? 1 : 0};
+  auto it = g.preds.find(key);
+  if (it != g.preds.end()) return it->second;
+  // coverage mode iff the space fits the exhaustive limit; otherwise the cap
+  // is the number of chains the reference DFS produced (predictor.cpp:107-131)
+  ag_predictor* p = nullptr;
+  check(ag_predictor_create(g.ctx, plan.exhaustive ? 0 : (int)plan.chains.size(),
+                            plan.exhaustive ? g.size : 0, &p));
+  int32_t nc = 0, len = 0, ex = 0, U = 0;
+  check(ag_predictor_info(p, &nc, &len, &ex, &U, nullptr));
+  std::vector<std::uint64_t> chains((size_t)nc * len);
+  check(ag_predictor_info(p, nullptr, nullptr, nullptr, nullptr, chains.data()));
+  bool same = nc == (int)plan.chains.size() && (ex != 0) == plan.exhaustive;
+  for (int c = 0; same && c < nc; ++c) {
+    same = (int)plan.chains[c].size() == len;
+    for (int k = 0; same && k < len; ++k)
+      same = chains[(size_t)c * len + k] == space.index_of(plan.chains[c][k]);
+  }
+  if (!same) {
+    ag_predictor_destroy(p);
+    throw std::logic_error("aragog_b200: GPU chain plan differs from the reference plan");
+  }
+  g.viable_cap = std::max(g.viable_cap, U);
+  g.preds.emplace(key, p);
+  return p;
+}
+
+}  // namespace
+
+namespace aragog {
+
+PredictionResult ConfigPredictor::predict(RequestId request, double budget) const {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const ConfigSpace& sp = space();
+  const RouterView rv = router_view(this->*get(PredRouter()));
+  Gpu& g = gpu_for(sp);
+  ag_predictor* p = predictor_for(g, sp, chains());
+  Truth t(rv.table->at(request), request, g.n, g.m);
+  std::vector<uint32_t> viable((size_t)std::max(g.viable_cap, 1));
+  int32_t nv = 0, se = 0, ve = 0;
+  double rt = 0.0;
+  uint8_t tr = 0;
+  check(ag_predict_host(p, &t.c, &rv.r, nullptr, budget, viable.data(), (int32_t)viable.size(), &nv,
+                        &se, &ve, &rt, &tr));
+  PredictionResult res;
+  res.viable.configs.reserve((size_t)nv);
+  for (int i = 0; i < nv; ++i) res.viable.configs.push_back(sp.at_index(viable[i]));
+  res.search_evals = se;
+  res.verify_evals = ve;
+  res.router_time = rt;
+  res.truncated = tr != 0;
+  return res;
+}
+
+std::vector<Configuration> enumerate_members(const AccurateSet& set, const ConfigSpace& space) {
+  if (!space.indexable() || space.size() > kEnumerableLimit) {
+    throw ValidationError("configuration space too large to enumerate");
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  Gpu& g = gpu_for(space);
+  Truth t(set, 0, g.n, g.m);
+  const ag_router oracle{AG_ROUTER_ORACLE, 0.0, 0.0, 0, 0.0};
+  std::uint64_t count = 0, off[2] = {0, 0}, total = 0;
+  std::vector<uint32_t> idx((size_t)g.size + 1);
+  check(ag_route_enumerate_host(g.ctx, &t.c, &oracle, 0, g.size, 0, &count, off, idx.data(), g.size,
+                                &total));
+  std::vector<Configuration> members;
+  members.reserve((size_t)total);
+  for (std::uint64_t i = 0; i < total; ++i) members.push_back(space.at_index(idx[i]));
+  return members;
+}
+
+Configuration select_per_input_config(const AccurateSet& accurate, const ConfigSpace& space,
+                                      PolicyKind kind, const RuntimeCostContext* ctx) {
+  // validation in the reference's order (workload.cpp:149-176, :129-147)
+  if (!space.indexable() || space.size() > kEnumerableLimit) {
+    throw ValidationError("configuration space too large to enumerate");
+  }
+  if (kind != PolicyKind::kPerInputStatic && kind != PolicyKind::kPerInputRuntimeCost) {
+    throw ValidationError("per-input selection needs a per-input policy kind");
+  }
+  std::vector<int32_t> occ, qa, slots;
+  std::vector<double> mean;
+  ag_load load{};
+  if (kind == PolicyKind::kPerInputRuntimeCost) {
+    if (ctx == nullptr) throw ValidationError("runtime-cost selection needs a load context");
+    if (ctx->service == nullptr) throw ValidationError("estimator needs services");
+    if (ctx->occupancy.size() != ctx->slots.size() || ctx->queued_ahead.size() != ctx->slots.size()) {
+      throw ValidationError("estimator context arrays disagree on tier count");
+    }
+    const int T = (int)ctx->slots.size();
+    occ.assign(ctx->occupancy.begin(), ctx->occupancy.end());
+    qa.assign(ctx->queued_ahead.begin(), ctx->queued_ahead.end());
+    slots.assign(ctx->slots.begin(), ctx->slots.end());
+    mean.assign(T, std::numeric_limits<double>::quiet_NaN());
+    // ServiceTimeModel::mean by the caller's libm (engine.cpp:62-65)
+    for (int m = 0; m < T && m < ctx->service->num_models(); ++m)
+      if (slots[m] > 0) mean[m] = ctx->service->mean(m);
+    load = ag_load{T, occ.data(), qa.data(), slots.data(), mean.data()};
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  Gpu& g = gpu_for(space);
+  Truth t(accurate, 0, g.n, g.m);
+  uint32_t chosen = 0;
+  double est = 0.0;
+  check(ag_select_per_input_host(
+      g.ctx, &t.c,
+      kind == PolicyKind::kPerInputStatic ? AG_POLICY_PER_INPUT_STATIC : AG_POLICY_PER_INPUT_RUNTIME_COST,
+      kind == PolicyKind::kPerInputRuntimeCost ? &load : nullptr, &chosen, &est));
+  return space.at_index(chosen);
+}
+
+Assignment beam_schedule(const std::vector<const Request*>& queue,
+                         const std::vector<EngineState>& engines, const SchedulerParams& params) {
+  if (params.beam_width < 1) throw ValidationError("beam width < 1");
+  // the tier range the queue and the pools use; digits are encoded over it
+  int max_model = 1;
+  for (const EngineState& e : engines) max_model = std::max(max_model, e.model);
+  const WorkflowGraph* graph = nullptr;
+  for (const Request* r : queue) {
+    if (!graph) graph = r->graph;
+    else if (r->graph != graph && r->graph->num_agents() != graph->num_agents())
+      throw ValidationError("GPU scheduler needs one workflow per round");
+    for (const Configuration& c : r->viable)
+      for (int d : c.models) max_model = std::max(max_model, d);
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  std::vector<int32_t> model, eslots, eocc;
+  std::vector<double> weight;
+  for (const EngineState& e : engines) {
+    model.push_back(e.model);
+    eslots.push_back(e.slots);
+    eocc.push_back(e.occupancy());
+    weight.push_back(e.weight);
+  }
+  ag_engines eg{(int32_t)engines.size(), model.data(), eslots.data(), eocc.data(), weight.data()};
+  int total_free = 0;
+  for (const EngineState& e : engines) total_free += std::max(0, e.slots - e.occupancy());
+  std::vector<ag_triple> trip((size_t)total_free + 1);
+  std::vector<int32_t> occ(std::max<size_t>(engines.size(), 1));
+  ag_assignment a{};
+  if (!graph) {
+    // no requests: the initial state, scored (scheduler.cpp:117-128, 248-287)
+    static const WorkflowGraph one = WorkflowGraph::build({"a"}, {});
+    graph = &one;
+  }
+  // a scheduling context for (graph, tiers): the costs are irrelevant here
+  const int M = max_model + 1;
+  std::vector<double> cost(M), thr(M);
+  for (int i = 0; i < M; ++i) {
+    cost[i] = 1.0 + i;
+    thr[i] = (double)(M - i);
+  }
+  Gpu& g = gpu_for(*graph, cost, thr);
+  const int N = g.n;
+  std::vector<uint64_t> ids;
+  std::vector<double> arrival;
+  std::vector<uint8_t> stages;
+  std::vector<int64_t> vptr{0};
+  std::vector<uint32_t> viable;
+  for (const Request* r : queue) {
+    ids.push_back(r->id);
+    arrival.push_back(r->arrival);
+    if ((int)r->stages.size() != N) throw ValidationError("request stage count mismatch");
+    for (StageState s : r->stages) stages.push_back((uint8_t)s);
+    for (const Configuration& c : r->viable) viable.push_back((uint32_t)index_of(c.models, M));
+    vptr.push_back((int64_t)viable.size());
+  }
+  if (viable.empty()) viable.push_back(0);
+  ag_queue q{(int32_t)queue.size(), ids.data(), arrival.data(), stages.data(), vptr.data(), viable.data()};
+  check(ag_beam_schedule(g.ctx, &q, &eg, params.beam_width, &a, trip.data(), (int32_t)trip.size(),
+                         occ.data()));
+  Assignment out;
+  out.triples.reserve((size_t)a.n_triples);
+  for (int i = 0; i < a.n_triples; ++i)
+    out.triples.push_back(AssignmentTriple{(std::size_t)trip[i].request_index, trip[i].request_id,
+                                           trip[i].agent, trip[i].model});
+  out.occupancy.assign(occ.begin(), occ.begin() + (long)engines.size());
+  out.utilization = a.utilization;
+  out.flexibility = a.flexibility;
+  out.skips = (long)a.skips;
+  out.states_explored = (std::size_t)a.states_explored;
+  return out;
+}
+
+}  // namespace aragog
+
+// kernels launched by the adapter's contexts (sim_trace reports it)
+extern "C" unsigned long long aragog_gpu_launches() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  unsigned long long n = 0;
+  for (auto& kv : cache()) n += ag_ctx_launch_count(kv.second->ctx);
+  return n;
+}

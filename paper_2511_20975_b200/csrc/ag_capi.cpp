@@ -202,6 +202,8 @@ void ag_ctx_destroy(ag_ctx* c) {
     cudaEventDestroy(r.stop);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->h_stage) cudaFreeHost(c->h_stage);
+  ag_sched_destroy(c->beam_cache);
   delete c;
 }
 
@@ -277,6 +279,96 @@ int ag_route_enumerate(ag_ctx* ctx, const ag_truth* truth, const ag_router* rout
   return agb::route_enumerate(ctx, truth, router, begin, end, flags, out);
 }
 
+}  // extern "C"
+
+namespace agb {
+// pinned staging for small host-path uploads (synchronised before reuse)
+int ensure_host_stage(ag_ctx* ctx, size_t bytes) {
+  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (ctx->h_stage && ctx->h_stage_bytes >= bytes) return AG_OK;
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+  ctx->h_stage = nullptr;
+  ctx->h_stage_bytes = 0;
+  const size_t b = std::max<size_t>(bytes, (size_t)1 << 16);
+  AG_CUDA(cudaMallocHost(&ctx->h_stage, b));
+  ctx->h_stage_bytes = b;
+  return AG_OK;
+}
+
+// Copies a host ag_truth batch into the context's device staging buffer in
+// one transfer (ids | seed_ptr | removed_ptr | removed | seeds) and returns
+// its device view.
+int upload_truth(ag_ctx* ctx, const ag_truth* th, ag_truth* td) {
+  const int R = th->n_requests;
+  const int n = ctx->space->n;
+  const size_t rows = (size_t)th->seed_ptr[R];
+  const size_t nrem = (size_t)th->removed_ptr[R];
+  const size_t o_ids = 0, o_sp = o_ids + 8 * (size_t)R, o_rp = o_sp + 4 * ((size_t)R + 1);
+  const size_t o_rem = (o_rp + 4 * ((size_t)R + 1) + 7) & ~(size_t)7;
+  const size_t o_seeds = o_rem + 8 * nrem;
+  const size_t bytes = o_seeds + rows * (size_t)n;
+  int rc;
+  if ((rc = ctx->h_truth.ensure(bytes))) return rc;
+  if ((rc = ensure_host_stage(ctx, bytes))) return rc;
+  char* h = (char*)ctx->h_stage;
+  std::memcpy(h + o_ids, th->request_ids, 8 * (size_t)R);
+  std::memcpy(h + o_sp, th->seed_ptr, 4 * ((size_t)R + 1));
+  std::memcpy(h + o_rp, th->removed_ptr, 4 * ((size_t)R + 1));
+  if (nrem) std::memcpy(h + o_rem, th->removed, 8 * nrem);
+  if (rows) std::memcpy(h + o_seeds, th->seeds, rows * (size_t)n);
+  char* d = (char*)ctx->h_truth.p;
+  AG_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  *td = ag_truth{R, (const uint64_t*)(d + o_ids), (const int32_t*)(d + o_sp),
+                 (const uint8_t*)(d + o_seeds), (const int32_t*)(d + o_rp),
+                 (const uint64_t*)(d + o_rem)};
+  return AG_OK;
+}
+}  // namespace agb
+
+extern "C" {
+
+// select_per_input_config for a batch of host AccurateSets: the members of
+// each set (oracle verdicts over the whole space, in canonical order) are
+// enumerated and compacted on the device, then re-costed and arg-minned there
+// (accuracy.cpp:227-238 + workload.cpp:149-176); only the choice comes back.
+int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* th, int32_t kind, const ag_load* load,
+                             uint32_t* chosen, double* est) {
+  if (!ctx || !th || !chosen) return fail(AG_ERR_VALIDATION, "null argument");
+  const int R = th->n_requests;
+  if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
+  if (R == 0) return AG_OK;
+  const ag_space* sp = ctx->space;
+  if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N <= 2^32 and N <= 32");
+  ag_truth td;
+  int rc = agb::upload_truth(ctx, th, &td);
+  if (rc) return rc;
+  const uint64_t S = sp->size;
+  const size_t W = (size_t)((S + 31) / 32);
+  if ((rc = ctx->counts.ensure(8 * (size_t)R)) || (rc = ctx->offsets.ensure(8 * ((size_t)R + 1))) ||
+      (rc = ctx->bitmap.ensure((size_t)R * W * 4 + 4)) || (rc = ctx->d_sel.ensure(16 * (size_t)R + 16)))
+    return rc;
+  const ag_router oracle{AG_ROUTER_ORACLE, 0.0, 0.0, 0, 0.0};
+  ag_route_out o1{(uint32_t*)ctx->bitmap.p, (uint64_t*)ctx->counts.p, (uint64_t*)ctx->offsets.p,
+                  nullptr, 0, nullptr};
+  if ((rc = agb::route_enumerate(ctx, &td, &oracle, 0, S, 0, &o1))) return rc;
+  uint64_t tot = 0;
+  AG_CUDA(cudaMemcpyAsync(&tot, (uint64_t*)ctx->offsets.p + R, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if ((rc = ctx->d_out_idx.ensure(4 * (size_t)tot + 4))) return rc;
+  if ((rc = agb::route_compact(ctx, R, 0, S, (const uint32_t*)ctx->bitmap.p,
+                               (const uint64_t*)ctx->offsets.p, (uint32_t*)ctx->d_out_idx.p, tot)))
+    return rc;
+  uint32_t* d_chosen = (uint32_t*)ctx->d_sel.p;
+  double* d_est = (double*)((char*)ctx->d_sel.p + ((4 * (size_t)R + 15) & ~(size_t)15));
+  if ((rc = ag_select_per_input(ctx, (const uint32_t*)ctx->d_out_idx.p, (const uint64_t*)ctx->offsets.p, R,
+                                kind, load, d_chosen, d_est)))
+    return rc;
+  AG_CUDA(cudaMemcpyAsync(chosen, d_chosen, 4 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));
+  if (est) AG_CUDA(cudaMemcpyAsync(est, d_est, 8 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));
+  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return AG_OK;
+}
+
 int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* th, const ag_router* router,
                             uint64_t begin, uint64_t end, uint32_t flags, uint64_t* counts,
                             uint64_t* offsets, uint32_t* indices, uint64_t capacity,
@@ -284,32 +376,16 @@ int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* th, const ag_router* ro
   if (!ctx || !th || !offsets || (th->n_requests > 0 && !counts))
     return fail(AG_ERR_VALIDATION, "null argument");
   const int R = th->n_requests;
-  const int n = ctx->space->n;
   if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
   if (R == 0) {
     offsets[0] = 0;
     if (total) *total = 0;
     return AG_OK;
   }
-  const size_t rows = (size_t)th->seed_ptr[R];
-  const size_t nrem = (size_t)th->removed_ptr[R];
-  // one staging block: ids | seed_ptr | removed_ptr | removed | seeds
-  const size_t o_ids = 0, o_sp = o_ids + 8 * (size_t)R, o_rp = o_sp + 4 * ((size_t)R + 1);
-  const size_t o_rem = (o_rp + 4 * ((size_t)R + 1) + 7) & ~(size_t)7;
-  const size_t o_seeds = o_rem + 8 * nrem;
-  const size_t bytes = o_seeds + rows * (size_t)n;
-  int rc;
-  if ((rc = ctx->h_truth.ensure(bytes))) return rc;
-  char* d = (char*)ctx->h_truth.p;
+  ag_truth td;
+  int rc = agb::upload_truth(ctx, th, &td);
+  if (rc) return rc;
   cudaStream_t s = ctx->stream;
-  AG_CUDA(cudaMemcpyAsync(d + o_ids, th->request_ids, 8 * (size_t)R, cudaMemcpyHostToDevice, s));
-  AG_CUDA(cudaMemcpyAsync(d + o_sp, th->seed_ptr, 4 * ((size_t)R + 1), cudaMemcpyHostToDevice, s));
-  AG_CUDA(cudaMemcpyAsync(d + o_rp, th->removed_ptr, 4 * ((size_t)R + 1), cudaMemcpyHostToDevice, s));
-  if (nrem) AG_CUDA(cudaMemcpyAsync(d + o_rem, th->removed, 8 * nrem, cudaMemcpyHostToDevice, s));
-  if (rows) AG_CUDA(cudaMemcpyAsync(d + o_seeds, th->seeds, rows * n, cudaMemcpyHostToDevice, s));
-  ag_truth td{R, (const uint64_t*)(d + o_ids), (const int32_t*)(d + o_sp),
-              (const uint8_t*)(d + o_seeds), (const int32_t*)(d + o_rp),
-              (const uint64_t*)(d + o_rem)};
   if ((rc = ctx->counts.ensure(8 * (size_t)R))) return rc;
   if ((rc = ctx->offsets.ensure(8 * ((size_t)R + 1)))) return rc;
   const uint64_t range = end > begin ? end - begin : 0;

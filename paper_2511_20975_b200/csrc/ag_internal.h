@@ -83,6 +83,10 @@ struct ag_ctx {
   // host-path staging
   agb::Scratch h_truth;
   agb::Scratch d_out_idx;
+  agb::Scratch d_sel;        // select_per_input host path: chosen / estimate
+  ag_sched* beam_cache = nullptr;  // session reused by stateless beam_schedule
+  void* h_stage = nullptr;   // pinned staging for host-path uploads
+  size_t h_stage_bytes = 0;
 };
 
 namespace agb {
@@ -103,5 +107,8 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r,
 int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32_t* bitmap,
                   const uint64_t* offsets, uint32_t* indices, uint64_t capacity);
 int make_router(const ag_router* r, RouterDev* out);
+// host ag_truth -> device view in the context's staging buffer
+int upload_truth(ag_ctx* ctx, const ag_truth* host, ag_truth* dev);
+int ensure_host_stage(ag_ctx* ctx, size_t bytes);
 
 }  // namespace agb

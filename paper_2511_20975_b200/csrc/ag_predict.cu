@@ -335,6 +335,7 @@ struct ag_predictor {
   uint32_t uid_top = 0;
   std::vector<uint64_t> chains_host;  // canonical indices [n_chains * len]
   agb::Scratch d_chain_uid, d_uniq_index, d_by_cost, d_by_index, d_scratch;
+  agb::Scratch d_out;  // ag_predict_host outputs
 };
 
 using agb::fail;
@@ -474,6 +475,45 @@ int ag_predict(ag_predictor* p, const ag_truth* t, const ag_router* router,
     agb::k_predict<<<blocks, agb::kPredWarps * 32, smem, ctx->stream>>>(a);
   }
   AG_CUDA(cudaGetLastError());
+  return AG_OK;
+}
+
+// The same with host buffers, copies included (the simulator drop-in path):
+// viable [R * viable_stride]; the other outputs optional.
+int ag_predict_host(ag_predictor* p, const ag_truth* th, const ag_router* router,
+                    const double* budgets, double budget_all, uint32_t* viable,
+                    int32_t viable_stride, int32_t* n_viable, int32_t* search_evals,
+                    int32_t* verify_evals, double* router_time, uint8_t* truncated) {
+  if (!p || !th || !viable || !n_viable || !router) return fail(AG_ERR_VALIDATION, "null argument");
+  ag_ctx* ctx = p->ctx;
+  const int R = th->n_requests;
+  if (R <= 0) return R == 0 ? AG_OK : fail(AG_ERR_VALIDATION, "negative request count");
+  if (viable_stride < 1) return fail(AG_ERR_VALIDATION, "viable_stride < 1");
+  ag_truth td;
+  int rc = agb::upload_truth(ctx, th, &td);
+  if (rc) return rc;
+  // device outputs: viable | n_viable | search | verify | router_time | budgets | truncated
+  const size_t o_v = 0;
+  const size_t o_n = o_v + 4 * (size_t)R * viable_stride;
+  const size_t o_s = o_n + 4 * (size_t)R, o_f = o_s + 4 * (size_t)R;
+  const size_t o_t = (o_f + 4 * (size_t)R + 7) & ~(size_t)7;
+  const size_t o_b = o_t + 8 * (size_t)R, o_u = o_b + 8 * (size_t)R;
+  const size_t bytes = o_u + (size_t)R;
+  if ((rc = p->d_out.ensure(bytes))) return rc;
+  char* d = (char*)p->d_out.p;
+  cudaStream_t s = ctx->stream;
+  if (budgets) AG_CUDA(cudaMemcpyAsync(d + o_b, budgets, 8 * (size_t)R, cudaMemcpyHostToDevice, s));
+  ag_predict_out o{(uint32_t*)(d + o_v), viable_stride, (int32_t*)(d + o_n), (int32_t*)(d + o_s),
+                   (int32_t*)(d + o_f), (double*)(d + o_t), (uint8_t*)(d + o_u)};
+  if ((rc = ag_predict(p, &td, router, budgets ? (const double*)(d + o_b) : nullptr, budget_all, &o)))
+    return rc;
+  AG_CUDA(cudaMemcpyAsync(n_viable, d + o_n, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
+  AG_CUDA(cudaMemcpyAsync(viable, d + o_v, 4 * (size_t)R * viable_stride, cudaMemcpyDeviceToHost, s));
+  if (search_evals) AG_CUDA(cudaMemcpyAsync(search_evals, d + o_s, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
+  if (verify_evals) AG_CUDA(cudaMemcpyAsync(verify_evals, d + o_f, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
+  if (router_time) AG_CUDA(cudaMemcpyAsync(router_time, d + o_t, 8 * (size_t)R, cudaMemcpyDeviceToHost, s));
+  if (truncated) AG_CUDA(cudaMemcpyAsync(truncated, d + o_u, (size_t)R, cudaMemcpyDeviceToHost, s));
+  AG_CUDA(cudaStreamSynchronize(s));
   return AG_OK;
 }
 

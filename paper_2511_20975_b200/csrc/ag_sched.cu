@@ -1658,6 +1658,23 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   return AG_OK;
 }
 
+// Empties a session for reuse (stateless beam_schedule): host mirror back to
+// its initial state; device arrays are rewritten by the next add before use.
+void reset_session(ag_sched* s) {
+  s->order.clear();
+  s->dirty_from = 0;
+  s->dead = 0;
+  s->quarantine.clear();
+  s->free_slots.clear();
+  for (int i = s->cap - 1; i >= 0; --i) s->free_slots.push_back(i);
+  std::fill(s->live.begin(), s->live.end(), 0);
+  std::fill(s->ready.begin(), s->ready.end(), 0);
+  s->npairs = 0;
+  s->upd_slot.clear();
+  s->upd_mask.clear();
+  s->pool_top = 0;
+}
+
 // deferred error of an asynchronous dispatch / add (read at round time)
 int check_async_status(ag_sched* s) {
   int32_t st = 0;
@@ -1932,20 +1949,36 @@ int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap, int64
   return AG_OK;
 }
 
-// Stateless beam_schedule: a throwaway session holding exactly this queue.
+// Stateless beam_schedule: the context's cached session, emptied, holds
+// exactly this queue (grown when a call needs more room).
 int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int beam_width,
                      ag_assignment* out, ag_triple* triples, int32_t triples_cap,
                      int32_t* occupancy) {
   if (!ctx || !q || !engines) return fail(AG_ERR_VALIDATION, "null argument");
   if (beam_width < 1) return fail(AG_ERR_VALIDATION, "beam width < 1");
   const int R = q->n_requests;
+  if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
   const uint64_t total = R > 0 ? (uint64_t)(q->viable_ptr[R] - q->viable_ptr[0]) : 0;
-  ag_sched* s = nullptr;
-  int rc = ag_sched_create(ctx, std::max(R, 1), std::max<uint64_t>(total, 1), &s);
-  if (rc) return rc;
-  std::vector<int32_t> slots(std::max(R, 1));
-  if ((rc = ag_sched_add(s, q, slots.data()))) {
+  ag_sched* s = ctx->beam_cache;
+  if (s && (s->cap < std::max(R, 1) || s->pool_cap < std::max<uint64_t>(total, 1))) {
+    const int cap = std::max(std::max(R, 1), 2 * s->cap);
+    const uint64_t pcap = std::max<uint64_t>(std::max<uint64_t>(total, 1), 2 * s->pool_cap);
     delete s;
+    ctx->beam_cache = s = nullptr;
+    int rc = ag_sched_create(ctx, cap, pcap, &s);
+    if (rc) return rc;
+    ctx->beam_cache = s;
+  } else if (!s) {
+    int rc = ag_sched_create(ctx, std::max(R, 64), std::max<uint64_t>(total, 1 << 14), &s);
+    if (rc) return rc;
+    ctx->beam_cache = s;
+  } else {
+    agb::reset_session(s);
+  }
+  std::vector<int32_t> slots(std::max(R, 1));
+  int rc = ag_sched_add(s, q, slots.data());
+  if (rc) {
+    agb::reset_session(s);
     return rc;
   }
   // container index per FIFO position; requests without ready stages keep
@@ -1957,7 +1990,6 @@ int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, 
   rc = agb::run_round(s, engines, beam_width, cidx.data(), out, triples, triples_cap, occupancy);
   if (rc == AG_OK && out)
     for (int i = 0; i < out->n_triples; ++i) triples[i].slot = -1;
-  delete s;
   return rc;
 }
 
