@@ -273,6 +273,46 @@ def run_deep(P, args, ws, rank, local, barrier):
             "timing": "host wall clock per sharded step, max over ranks, median of steps"}
 
 
+INTEG = os.path.join(ROOT, "integration", "_build")
+C5_RATES = (0.5, 1.5, 2.5, 3.5)
+
+
+def run_config5(horizon=240.0):
+    """Config 5: the reference simulator (run_simulation, reference.json) over
+    the shipped sweep rates in horizon mode, built twice from the unmodified
+    sources -- plain, and relinked with the GPU adapter (predict, beam
+    rounds, per-input selection on the B200; integration/Makefile).  Reports
+    wall-clock scheduling rounds/s of both builds and whether the JSONL traces
+    are byte-identical."""
+    ref_bin, gpu_bin = os.path.join(INTEG, "sim_trace_ref"), os.path.join(INTEG, "sim_trace_gpu")
+    scen = os.path.join(INTEG, "proj", "scenarios", "reference.json")
+    if not (os.path.exists(ref_bin) and os.path.exists(gpu_bin) and os.path.exists(scen)):
+        return None
+    pts, same = [], True
+    with tempfile.TemporaryDirectory() as td:
+        for rate in C5_RATES:
+            row = {"rate": rate}
+            outs = []
+            for kind, b in (("reference", ref_bin), ("gpu", gpu_bin)):
+                out = os.path.join(td, f"{kind}_{rate}.jsonl")
+                r = subprocess.run([b, scen, "aragog", out, "--horizon", str(horizon), "--rate",
+                                    str(rate)], capture_output=True, text=True, check=True)
+                j = json.loads(r.stdout.strip().splitlines()[-1])
+                row[kind] = {"rounds": j["rounds"], "requests": j["requests"],
+                             "wall_s": j["wall_s"], "rounds_per_s": j["rounds_per_s"],
+                             "gpu_launches": j["gpu_launches"]}
+                outs.append(open(out, "rb").read())
+            row["trace_identical"] = outs[0] == outs[1]
+            same &= row["trace_identical"]
+            pts.append(row)
+    return {"workload": f"config5: reference.json under run_simulation, horizon {horizon:g} s, "
+                        f"aragog policy, rates {list(C5_RATES)} req/s; reference build vs the "
+                        "same sources relinked with the GPU adapter",
+            "traces_identical": same, "points": pts,
+            "note": "single-request decisions through the C ABI: each predict / round is one "
+                    "launch + synchronisation, so tiny queues are launch-latency bound"}
+
+
 def run_ours(args):
     import torch
 
@@ -366,6 +406,7 @@ def run_ours(args):
 
     sched = run_sched(P, W, dev, args) if rank == 0 and not args.no_sched else None
     deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)
+    config5 = run_config5() if rank == 0 and not args.no_config5 else None
     clk = clocks.stop()
 
     if rank != 0:
@@ -407,6 +448,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "sched": sched,
         "deep": deep,
+        "config5": config5,
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
@@ -427,6 +469,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
     ap.add_argument("--no-deep", action="store_true")
+    ap.add_argument("--no-config5", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
