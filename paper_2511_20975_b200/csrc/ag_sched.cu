@@ -628,21 +628,21 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     // the next candidate of the current request is visited unconditionally;
     // otherwise the next candidate whose mask meets a free engine
     int found = -1;
-    if (last_q >= 0 && wait_for((unsigned)j) > (unsigned)j && recf(j).qi == last_q) {
-      found = j;
-    } else {
-      for (int j0 = j;;) {
-        const unsigned h = wait_for((unsigned)j0);
-        if (h <= (unsigned)j0) break;  // producers done, list exhausted
-        const int jj = j0 + lane;
-        const bool ok = jj < (int)h && (maskf(jj) & U) != 0;
-        const uint32_t b = __ballot_sync(kFull, ok);
-        if (b) {
-          found = j0 + __ffs(b) - 1;
-          break;
-        }
-        j0 = min(j0 + 32, (int)h);
+    uint32_t base = 0;
+    for (int j0 = j;;) {
+      const unsigned h = wait_for((unsigned)j0);
+      if (h <= (unsigned)j0) break;  // producers done, list exhausted
+      const int jj = j0 + lane;
+      const uint32_t mm = jj < (int)h ? maskf(jj) : 0u;
+      const bool cont = lane == 0 && j0 == j && last_q >= 0 && recf(j).qi == last_q;
+      const uint32_t b = __ballot_sync(kFull, (mm & U) != 0 || cont);
+      if (b) {
+        const int src = __ffs(b) - 1;
+        found = j0 + src;
+        base = __shfl_sync(kFull, mm, src);
+        break;
       }
+      j0 = min(j0 + 32, (int)h);
     }
     { const long long t = clock64(); tw[0] += t - tp; tp = t; }
     if (found < 0) break;
@@ -657,7 +657,6 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       pi = (long long)cr.pos + 1;
     }
     const int qcur = cr.qi, a = (int)(cr.slot_agent >> 26), slot = (int)(cr.slot_agent & 0x3ffffffu);
-    const uint32_t base = maskf(j);
     const double initial = (double)cr.nvia;
     const int hrow = j;
     if (hrow >= rows && hrow < A.hist_cap) rows = ld_acquire(&s_rows);  // uniform
@@ -711,10 +710,13 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     // candidate contributes one skip child (scheduler.cpp:331-349).
     // Exclusive offsets of the per-state child counts (<= 33) by bit slices.
     const int my_n = lane < nst ? (mk ? __popc(mk) : 1) : 0;
-    int off = 0;
+    int off = 0, nchild = 0;
 #pragma unroll
-    for (int bit = 0; bit < 6; ++bit) off += __popc(__ballot_sync(kFull, (my_n >> bit) & 1) & lt) << bit;
-    const int nchild = __shfl_sync(kFull, off + my_n, 31);
+    for (int bit = 0; bit < 6; ++bit) {
+      const uint32_t bb = __ballot_sync(kFull, (my_n >> bit) & 1);
+      off += __popc(bb & lt) << bit;
+      nchild += __popc(bb) << bit;
+    }
     explored += (unsigned long long)nchild;
     ++n_steps;
     n_child += nchild;
@@ -812,20 +814,23 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         }
       }
       // nested retention (scheduler.cpp:351-370): level w adopts the best
-      // unused child of parents < w
-      bool used = false;
+      // unused child of parents < w -- the lowest rank not yet taken in the
+      // union of the parents' rank masks
+      if (valid) s_picked[rank] = lane;  // rank -> child lane
+      uint32_t avail_ranks = 0, taken = 0;
+      int myrank = 0;
+#pragma unroll 4
       for (int w = 1; w <= B && npick < nchild; ++w) {
-        const bool el = valid && !used && par < w;
-        const unsigned m = __reduce_min_sync(kFull, el ? rank : 0xffffffffu);
-        if (m == 0xffffffffu) continue;
-        if (el && rank == m) {
-          used = true;
-          s_picked[npick] = lane;
-        }
+        avail_ranks |= __reduce_or_sync(kFull, (valid && par == w - 1) ? 1u << rank : 0u);
+        const uint32_t av = avail_ranks & ~taken;
+        if (!av) continue;
+        const int r = __ffs(av) - 1;
+        taken |= 1u << r;
+        if (lane == npick) myrank = r;
         ++npick;
       }
       __syncwarp();
-      const int src = lane < npick ? s_picked[lane] : 0;
+      const int src = lane < npick ? s_picked[myrank] : 0;
       c_u = __shfl_sync(kFull, cu, src);
       c_fs = __shfl_sync(kFull, cfs, src);
       c_fc = __shfl_sync(kFull, cfc, src);
@@ -932,6 +937,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     const int p_ln = __shfl_sync(kFull, st_ln, c_par);
     const bool mknode = c_eng >= 0;
     const uint32_t nb = __ballot_sync(kFull, mknode);
+    if (nnodes + __popc(nb) > A.max_nodes) wstatus = AG_ERR_INTERNAL + 300;  // history overflow (uniform)
     const int c_mdl = mknode ? e_model[c_eng] : 0;
     const uint64_t mykey = mknode ? key_base | (uint64_t)(uint32_t)c_mdl : kEnd;
     // occupancy rows of the new states: lane (w, e) copies engine e of state w
@@ -951,7 +957,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       if (mknode) {
         if (s_occ[cur][c_par][c_eng] + 1 >= e_slots[c_eng]) st_fm &= ~(1u << c_eng);
         const int id = nnodes + __popc(nb & lt);
-        if (id < A.max_nodes) {
+        if (!wstatus) {
           Node nd;
           nd.qi = qcur;
           nd.am = (a << 8) | c_mdl;
@@ -963,8 +969,6 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
           nd.pad = 0;
           if (id < kSmemNodes) s_nodes[id] = nd;
           else A.gnodes[id - kSmemNodes] = nd;
-        } else {
-          wstatus = AG_ERR_INTERNAL + 300;  // history overflow
         }
         st_nd = id;
         st_lq = qcur;
@@ -987,7 +991,6 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       }
     }
     nnodes += __popc(nb);
-    wstatus = (int)__reduce_max_sync(kFull, (unsigned)wstatus);
     __syncwarp();
     cur = nxt;
     nst = npick;
