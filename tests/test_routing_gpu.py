@@ -171,3 +171,33 @@ def test_reference_enumerate_members_guard():
     assert P.enumerate_members(space, [[1, 0]]) == [[1, 0], [1, 1], [1, 2], [2, 0], [2, 1], [2, 2]]
     with pytest.raises(P.ValidationError):
         P.enumerate_members(P.ConfigSpace.chain(7, 4), [[0] * 7])
+
+
+@pytest.mark.parametrize("shift", [1, 2, 3])
+@pytest.mark.parametrize("cap_cut", [0, 1, 5, 777])
+def test_compaction_unaligned_output_and_partial_capacity(shift, cap_cut):
+    """k_route_compact writes 16-byte vectors at the output's own phase: an
+    output pointer off 16-byte alignment and a capacity that ends inside a
+    vector must still give exactly the canonical members up to capacity and
+    leave everything past it untouched."""
+    space = P.ConfigSpace.chain(5, 4)
+    batch = P.AccuracyBatch.generate(space, P.GenParams(), 37, seed=11)
+    dev = P.Device(space)
+    router = P.OracleRouter()
+    full = dev.route_enumerate(batch.to_device(), router)
+    torch.cuda.synchronize()
+    total = int(full.offsets[-1])
+    want = full.indices[:total].clone()
+    cap = total - cap_cut
+    sentinel = -7
+    big = torch.full((cap + shift + 64,), sentinel, dtype=torch.int32, device=want.device)
+    out = dev.alloc_route(batch.n_requests, 0, space.size, cap)
+    out["indices"] = big[shift:]
+    out["capacity"] = cap
+    dev.route_enumerate(batch.to_device(), router, out=out)
+    torch.cuda.synchronize()
+    got = big[shift:shift + cap]
+    assert torch.equal(got, want[:cap])
+    assert int((big[:shift] != sentinel).sum()) == 0
+    assert int((big[shift + cap:] != sentinel).sum()) == 0
+    assert int(out["overflow"][0]) == (1 if cap_cut else 0)
