@@ -336,6 +336,17 @@ int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* truth_host,
                              int32_t kind, const ag_load* load,
                              uint32_t* chosen, double* est);
 
+/* select_per_workflow_config(sample, space, tolerance) (workload.cpp:99-127)
+ * without the reference's 4096-configuration guard: sample = a batch of host
+ * AccurateSets; chosen receives the canonical index of the first
+ * configuration in (static cost, index) order that is accurate on at least
+ * (1 - tolerance) * |sample| sets, hits (optional) its count.  Every set is
+ * scored over the whole space on the device, counts are column popcounts of
+ * the verdict bitmap, the choice a (cost, index) min-reduction. */
+int ag_select_per_workflow_host(ag_ctx* ctx, const ag_truth* sample_host,
+                                double tolerance, uint64_t* chosen,
+                                uint64_t* hits);
+
 /* snapshot_load's queued_ahead (simulation.cpp:194-213): per model tier, the
  * number of ready (request, agent) pairs of the session whose candidate set
  * contains the tier.  out [M] host. */

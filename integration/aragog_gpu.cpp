@@ -8,8 +8,9 @@
 //   beam_schedule                 (src/scheduler.cpp:289-378) -> ag_beam_schedule
 //   enumerate_members             (src/accuracy.cpp:227-238)  -> ag_route_enumerate_host
 //   select_per_input_config       (src/workload.cpp:149-176)  -> ag_select_per_input_host
+//   select_per_workflow_config    (src/workload.cpp:99-127)   -> ag_select_per_workflow_host
 //
-// The reference objects are linked with these four symbols weakened
+// The reference objects are linked with these five symbols weakened
 // (objcopy --weaken-symbol, integration/Makefile), so the definitions below
 // win at link time.  There is no CPU fallback: a RouterBackend that is not an
 // OracleRouter (or a NoisyRouter over one) -- e.g. the CountingRouter test
@@ -319,6 +320,36 @@ Configuration select_per_input_config(const AccurateSet& accurate, const ConfigS
       g.ctx, &t.c,
       kind == PolicyKind::kPerInputStatic ? AG_POLICY_PER_INPUT_STATIC : AG_POLICY_PER_INPUT_RUNTIME_COST,
       kind == PolicyKind::kPerInputRuntimeCost ? &load : nullptr, &chosen, &est));
+  return space.at_index(chosen);
+}
+
+Configuration select_per_workflow_config(const std::vector<AccurateSet>& sample,
+                                         const ConfigSpace& space, double tolerance) {
+  // validation in the reference's order (workload.cpp:102-108)
+  if (sample.empty()) throw ValidationError("per-workflow sample is empty");
+  if (tolerance < 0 || tolerance > 1) throw ValidationError("tolerance outside [0, 1]");
+  if (!space.indexable() || space.size() > kEnumerableLimit) {
+    throw ValidationError("configuration space too large to enumerate");
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  Gpu& g = gpu_for(space);
+  std::vector<std::uint64_t> ids(sample.size());
+  std::vector<int32_t> sp{0}, rp{0};
+  std::vector<uint8_t> seeds;
+  std::vector<std::uint64_t> removed;
+  for (std::size_t i = 0; i < sample.size(); ++i) {
+    ids[i] = i;
+    for (const Configuration& s : sample[i].seeds) {
+      if ((int)s.models.size() != g.n) throw ValidationError("configuration length mismatch");
+      for (int d : s.models) seeds.push_back((uint8_t)d);
+    }
+    for (const Configuration& r : sample[i].removed) removed.push_back(index_of(r.models, g.m));
+    sp.push_back(sp.back() + (int32_t)sample[i].seeds.size());
+    rp.push_back(rp.back() + (int32_t)sample[i].removed.size());
+  }
+  const ag_truth t{(int32_t)sample.size(), ids.data(), sp.data(), seeds.data(), rp.data(), removed.data()};
+  std::uint64_t chosen = 0, hits = 0;
+  check(ag_select_per_workflow_host(g.ctx, &t, tolerance, &chosen, &hits));
   return space.at_index(chosen);
 }
 

@@ -231,6 +231,35 @@ def select_per_input(n, m, cost, occupancy, queued, slots, mean, kind, members):
     return int(chosen.value), est.value
 
 
+def select_per_workflow(n, m, cost, tb, tolerance=0.0):
+    """select_per_workflow_config (reference src/workload.cpp:99-127), restated:
+    every configuration in (static cost, canonical index) order -- the cost a
+    left fold in agent order (workflow.cpp:291-296) -- and the first one
+    accurate on at least (1 - tolerance) * |sample| sets.  The membership
+    verdicts come from the C restatement's enumerate (AccurateSet::contains).
+    Test infrastructure only."""
+    R = len(tb.request_ids)
+    if R == 0:
+        raise ValueError("per-workflow sample is empty")
+    S = m ** n
+    hits = np.zeros(S, np.int64)
+    for r in range(R):
+        cnt, words = enumerate_bitmap(tb, Router(ORACLE, 0, 0, 0, 0), r, 0, S)
+        bits = np.unpackbits(np.asarray(words, np.uint32).view(np.uint8), bitorder="little")[:S]
+        hits += bits
+    costs = np.zeros(S)
+    idx = np.arange(S, dtype=np.int64)
+    for a in range(n):  # agent order, left fold
+        digit = (idx // (m ** (n - 1 - a))) % m
+        costs = costs + np.asarray(cost, np.float64)[digit]
+    needed = (1.0 - tolerance) * float(R)
+    order = np.lexsort((idx, costs))
+    for c in order:
+        if float(hits[c]) >= needed:
+            return int(c), int(hits[c])
+    raise ValueError("per-workflow scan found no configuration")
+
+
 class QueueData:
     """Flat queue view (the reference's vector<const Request*>) + engine pools."""
 

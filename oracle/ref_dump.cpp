@@ -520,10 +520,50 @@ json dump_workload() {
   return out;
 }
 
+// ----------------------------------------------------------- per-workflow
+// select_per_workflow_config (workload.cpp:99-127) over generated samples,
+// including violation-injected (removed-list) sets on small spaces.
+json dump_workflow() {
+  json out = json::array();
+  const int shapes[][2] = {{1, 2}, {2, 3}, {3, 3}, {3, 4}, {4, 3}, {5, 4}, {6, 4}};
+  const std::size_t counts[] = {1, 7, 40};
+  const double tols[] = {0.0, 0.1, 0.35};
+  const double viols[] = {0.0, 0.05};
+  std::uint64_t seed = 900;
+  for (auto& sh : shapes) {
+    WorkflowGraph g = chain_graph(sh[0]);
+    ModelCatalog cat = geometric_catalog(sh[1]);
+    ConfigSpace space(g, cat);
+    json costs = json::array();
+    for (int i = 0; i < sh[1]; ++i) costs.push_back(cat.at(i).cost);
+    for (double v : viols)
+      for (std::size_t cnt : counts) {
+        AccuracyGenParams ap;
+        ap.violation_rate = v;
+        ++seed;
+        AccuracyTable table = generate_accuracy_table(space, ap, cnt, seed);
+        std::vector<AccurateSet> sample;
+        for (RequestId id = 0; id < cnt; ++id) sample.push_back(table.at(id));
+        for (double tol : tols) {
+          Configuration pick = select_per_workflow_config(sample, space, tol);
+          out.push_back({{"n", sh[0]}, {"m", sh[1]}, {"cost", costs}, {"seed", seed},
+                         {"count", cnt}, {"violation_rate", v}, {"tolerance", tol},
+                         {"pick", space.index_of(pick)}});
+        }
+      }
+  }
+  return out;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   std::string dir = argc > 1 ? argv[1] : ".";
+  if (argc > 2 && std::string(argv[2]) == "workflow") {
+    write(dir, "workflow.json", dump_workflow());
+    return 0;
+  }
+  write(dir, "workflow.json", dump_workflow());
   write(dir, "rng.json", dump_rng());
   write(dir, "graph.json", dump_graphs());
   write(dir, "truth.json", dump_truth());

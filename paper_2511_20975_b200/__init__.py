@@ -6,4 +6,5 @@ from .routing import (AccuracyBatch, ConfigSpace, Device, DeviceAccuracyBatch,  
                       GenParams, NoisyRouter, OracleRouter, RouteResult, enumerate_members)
 from .predictor import ConfigPredictor, PredictionBatch  # noqa: F401,E402
 from .scheduler import (PER_INPUT_RUNTIME_COST, PER_INPUT_STATIC, Assignment, Engines, Queue,  # noqa: F401,E402
-                        RuntimeCostContext, SchedSession, beam_schedule, select_per_input)
+                        RuntimeCostContext, SchedSession, beam_schedule, select_per_input,
+                        select_per_workflow)

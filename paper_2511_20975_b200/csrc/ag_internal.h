@@ -84,6 +84,7 @@ struct ag_ctx {
   agb::Scratch h_truth;
   agb::Scratch d_out_idx;
   agb::Scratch d_sel;        // select_per_input host path: chosen / estimate
+  agb::Scratch wf_hits, wf_best;  // select_per_workflow: hit counts, block minima
   ag_sched* beam_cache = nullptr;  // session reused by stateless beam_schedule
   void* h_stage = nullptr;   // pinned staging for host-path uploads
   size_t h_stage_bytes = 0;

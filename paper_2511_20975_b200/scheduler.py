@@ -225,6 +225,18 @@ def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_CO
     return chosen[:R], est[:R]
 
 
+def select_per_workflow(device: Device, sample, tolerance: float = 0.0):
+    """select_per_workflow_config(sample, space, tolerance) (workload.cpp:99-127)
+    over a host AccuracyBatch, without the 4096-configuration guard: returns
+    (canonical index, accurate count over the sample)."""
+    chosen = C.c_uint64()
+    hits = C.c_uint64()
+    t = sample.c_struct()
+    check(lib().ag_select_per_workflow_host(device.handle, C.byref(t), C.c_double(tolerance),
+                                            C.byref(chosen), C.byref(hits)))
+    return int(chosen.value), int(hits.value)
+
+
 def _queued_ahead(self) -> list:
     """snapshot_load's queued_ahead per model tier (simulation.cpp:194-213)."""
     out = np.zeros(64, np.int32)

@@ -30,7 +30,8 @@ def _run(binary, scenario, policy, out, *opts):
 @need
 @pytest.mark.parametrize("scenario", ["reference.json", "reference_noisy.json", "mm1.json",
                                       "decompose.json"])
-@pytest.mark.parametrize("policy", ["aragog", "per-input-static", "per-input-runtime-cost"])
+@pytest.mark.parametrize("policy", ["aragog", "per-workflow", "per-input-static",
+                                    "per-input-runtime-cost"])
 def test_trace_byte_identical(tmp_path, scenario, policy):
     ref = str(tmp_path / "ref.jsonl")
     gpu = str(tmp_path / "gpu.jsonl")
