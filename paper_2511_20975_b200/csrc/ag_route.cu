@@ -284,15 +284,33 @@ struct ScoreArgs {
   uint32_t flags;
   uint64_t H;        // SWAR high-bit mask over N-2 bytes
   int path2d;        // 2-D mask path available for this space
+  int pat_lg;        // phase-pattern path: log2 gcd(M*M, 32), -1 = unavailable
+  int pat_P;         // phases per block (M*M / gcd)
   const uint32_t* colmask;
   uint32_t* bitmap;  // [R * W]
   uint32_t* task_counts;
+};
+
+// Phase-pattern path (M*M >= 32 and few phases): a 32-index word starting at
+// block offset o (block = the M*M indices sharing digits 0..N-3) holds the
+// same (x, l) digit pattern for every block, so the verdict word of a seed s
+// is lo(s, o) when s.Q <= Q plus hi(s, o) when s.Q <= Q + 1 (the part of the
+// word that runs into the next block).  Offsets of the words of a request
+// form P = M*M / gcd(M*M, 32) phases, tabulated per warp-task once; a word
+// then costs two SWAR prefix tests and two ORs per seed.
+constexpr int kPatSeeds = 4;
+constexpr int kPatMax = 32;
+
+struct PatTable {
+  uint32_t lo[kPatSeeds][kPatMax];
+  uint32_t hi[kPatSeeds][kPatMax];
 };
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   __shared__ PackedSeeds s_seeds[kWarpsPerBlock];
   __shared__ uint32_t s_tr[kWarpsPerBlock][32][33];
+  __shared__ PatTable s_pat[kWarpsPerBlock];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t task = blockIdx.x * kWarpsPerBlock + wid;
   if ((uint64_t)task >= (uint64_t)a.R * a.C) return;
@@ -332,7 +350,62 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   // all 32 words of this lane are full and inside [begin, end)
   const bool full = (uint64_t)i0s + 1024 <= a.end && wl + 32 <= wend;
   const bool extras = (r1 > r0) || a.rt.kind == AG_ROUTER_NOISY || (a.flags & AG_FORCE_TOP);
-  if (fast && full && !extras) {
+  const bool pat = fast && !extras && a.pat_lg >= 0 && k <= kPatSeeds;
+  if (pat) {
+    // phase tables of this task's seeds: lanes own (seed, phase) entries
+    const uint32_t Bq = m * m, g = 1u << a.pat_lg;
+    const uint32_t r0 = (uint32_t)(a.begin % g);  // every word offset is = r0 (mod g)
+    // one (seed, phase) entry per pass, lane = bit position
+    for (int s = 0; s < k; ++s) {
+      const uint32_t sx = s_seeds[wid].xl[s] >> 8, sl = s_seeds[wid].xl[s] & 0xFFu;
+      for (int p = 0; p < a.pat_P; ++p) {
+        uint32_t t = r0 + g * (uint32_t)p + (uint32_t)lane;
+        const bool nxt = t >= Bq;
+        if (nxt) t -= Bq;
+        const uint32_t x = divm(t, a.sp.div_m), l = t - x * m;
+        const bool in = x >= sx && l >= sl;
+        const uint32_t lo = __ballot_sync(0xffffffffu, in && !nxt);
+        const uint32_t hi = __ballot_sync(0xffffffffu, in && nxt);
+        if (lane == 0) {
+          s_pat[wid].lo[s][p] = lo;
+          s_pat[wid].hi[s][p] = hi;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (pat && full) {
+    // hot path: oracle router, no removals, 32 full words, phase tables
+    const WordPos p0 = word_pos(a.sp, i0s);
+    const uint32_t Bq = m * m;
+    uint32_t o = p0.x * m + p0.l0;
+    uint64_t Q = p0.Q, Qn = q_add(p0.Q, 1, m, nq);
+    const int lg = a.pat_lg;
+    const PatTable& pt = s_pat[wid];
+    uint64_t sq[kPatSeeds];
+#pragma unroll
+    for (int s = 0; s < kPatSeeds; ++s) sq[s] = s < k ? s_seeds[wid].q[s] : ~0ull;
+#pragma unroll 4
+    for (uint32_t it = 0; it < 32; ++it) {
+      const uint32_t ph = o >> lg;
+      uint32_t word = 0;
+#pragma unroll
+      for (int s = 0; s < kPatSeeds; ++s) {
+        if (s < k) {
+          if ((((Q | a.H) - sq[s]) & a.H) == a.H) word |= pt.lo[s][ph];
+          if ((((Qn | a.H) - sq[s]) & a.H) == a.H) word |= pt.hi[s][ph];
+        }
+      }
+      o += 32;
+      if (o >= Bq) {
+        o -= Bq;
+        Q = Qn;
+        Qn = q_add(Qn, 1, m, nq);
+      }
+      cnt += __popc(word);
+      s_tr[wid][lane][it] = word;
+    }
+  } else if (fast && full && !extras) {
     // hot path: oracle router, no removals, 32 full words
     WordPos pos = word_pos(a.sp, i0s);
 #pragma unroll 4
@@ -751,6 +824,14 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   a.H = 0;
   for (int b = 0; b < sp->n - 2 && b < 8; ++b) a.H |= 0x80ull << (8 * b);
   a.path2d = (sp->n >= 2 && sp->n - 2 <= 8 && sp->m <= 32) ? 1 : 0;
+  {
+    // phase-pattern path: blocks of >= 32 indices, <= kPatMax phases
+    const uint32_t Bq = (uint32_t)sp->m * (uint32_t)sp->m;
+    uint32_t g = 1;
+    while (g < 32 && Bq % (2 * g) == 0) g *= 2;
+    a.pat_P = (int)(Bq / g);
+    a.pat_lg = (a.path2d && Bq >= 32 && a.pat_P <= kPatMax) ? __builtin_ctz(g) : -1;
+  }
   a.colmask = (const uint32_t*)ctx->colmask.p;
   a.bitmap = bitmap;
   a.task_counts = (uint32_t*)ctx->chunk_counts.p;
