@@ -204,22 +204,31 @@ def run_sched(P, W, dev, args):
     """Config 3 on this GPU: p50/p99 of the C-ABI round latency."""
     c3 = W.Config3(dev, inflight=SCHED_INFLIGHT, rounds=args.sched_rounds + args.sched_warmup,
                    seed=SEED, beam=SCHED_BEAM)
-    dev_us, capi_us = [], []
+    dev_us, capi_us, free = [], [], []
+    weights = list(c3.space.slot_throughput)
 
     def on_round(rd, a):
         if rd >= args.sched_warmup:
             t = c3.sess.round_timing()
             dev_us.append(float(t.sum()))
             capi_us.append(c3.sess.last_round_us())
+            free.append(W.config3_engines(rd, SEED, weights)[1])
 
     _, h, assigned = c3.run(on_round=on_round)
     capi = np.asarray(capi_us)
     devt = np.asarray(dev_us)
+    free = np.asarray(free)
+    by_free = {}
+    for f in sorted(set(free.tolist())):
+        sel = capi[free == f]
+        by_free[str(f)] = {"rounds": int(sel.size), "p50_us": float(np.percentile(sel, 50)),
+                           "p99_us": float(np.percentile(sel, 99))}
     return {"p50_us": float(np.percentile(capi, 50)), "p99_us": float(np.percentile(capi, 99)),
             "mean_us": float(capi.mean()),
             "device_p50_us": float(np.percentile(devt, 50)),
             "device_p99_us": float(np.percentile(devt, 99)),
             "rounds": len(capi), "warmup_rounds": args.sched_warmup, "assigned": int(assigned),
+            "by_free_slots": by_free,
             "decision_hash": f"{h:016x}",
             "what": "ag_sched_round wall time inside the C ABI (update upload + round kernel + "
                     "assignment download); device = the round kernel alone"}
