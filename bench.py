@@ -413,6 +413,35 @@ def run_ours(args):
     e2e_ok = int(hb_offsets[-1]) == total_members
     P.lib().ag_host_free(pinned)
 
+    # the same batch with the noisy router of BASELINE config 2 (fp 0, fn 0.3,
+    # seed 7): integer-issue bound (two splitmix64 per needed configuration)
+    noisy = None
+    if not args.no_noisy:
+        nrouter = P.NoisyRouter(0.0, 0.3, 7)
+        nprobe = dev.route_enumerate(truth, nrouter, compact=False)
+        torch.cuda.synchronize()
+        nmem = int(nprobe.offsets[-1])
+        nout = dev.alloc_route(REQUESTS_PER_GPU, 0, S, nmem)
+        for _ in range(2):
+            dev.route_enumerate(truth, nrouter, out=nout)
+        nev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(3)]
+        barrier()
+        dev.profile_begin()
+        for i in range(3):
+            flush.fill_(i & 0xFF)
+            nev[i][0].record(stream)
+            dev.route_enumerate(truth, nrouter, out=nout)
+            nev[i][1].record(stream)
+        nprof = dev.profile_end()
+        barrier()
+        nms = [x.elapsed_time(y) for x, y in nev]
+        noisy = {"router": "NoisyRouter(fp 0, fn 0.3, seed 7)",
+                 "configs_per_s": REQUESTS_PER_GPU * S / (statistics.median(nms) / 1e3),
+                 "ms_per_step": statistics.median(nms), "members_per_step": nmem,
+                 "kernel_ms": {k: v[0] / v[1] for k, v in nprof.items()},
+                 "bound": "integer issue (k_route_score)"}
+        del nout, nprobe
     sched = run_sched(P, W, dev, args) if rank == 0 and not args.no_sched else None
     deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)
     config5 = run_config5() if rank == 0 and not args.no_config5 else None
@@ -457,6 +486,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "sched": sched,
         "deep": deep,
+        "noisy": noisy,
         "config5": config5,
         "clocks": clk,
     }
@@ -479,6 +509,7 @@ def main():
     ap.add_argument("--no-sched", action="store_true")
     ap.add_argument("--no-deep", action="store_true")
     ap.add_argument("--no-config5", action="store_true")
+    ap.add_argument("--no-noisy", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

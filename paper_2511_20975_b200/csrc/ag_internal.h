@@ -78,6 +78,8 @@ struct ag_ctx {
   // routing scratch
   agb::Scratch chunk_counts, chunk_off, bitmap, counts, offsets, overflow;
   agb::Scratch colmask;  // per-space last-digit masks (route 2-D path)
+  agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
+  bool hc_ready = false;
   agb::Scratch cost_args, cost_status;  // runtime-cost argmin
   int colmask_m = 0;
   // host-path staging

@@ -287,6 +287,7 @@ struct ScoreArgs {
   int pat_lg;        // phase-pattern path: log2 gcd(M*M, 32), -1 = unavailable
   int pat_P;         // phases per block (M*M / gcd)
   const uint32_t* colmask;
+  const uint64_t* hc;  // hash_config(c) per canonical index (noisy router), or null
   uint32_t* bitmap;  // [R * W]
   uint32_t* task_counts;
 };
@@ -310,7 +311,10 @@ template <int NT>
 __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   __shared__ PackedSeeds s_seeds[kWarpsPerBlock];
   __shared__ uint32_t s_tr[kWarpsPerBlock][32][33];
+  // phase tables (truth words), then reused as the noise pass's list of
+  // needed bits of half a group (512 x u16 = the table's 1 KB)
   __shared__ PatTable s_pat[kWarpsPerBlock];
+  static_assert(sizeof(PatTable) >= 512 * sizeof(uint16_t), "needed-bit list overlays the phase table");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t task = blockIdx.x * kWarpsPerBlock + wid;
   if ((uint64_t)task >= (uint64_t)a.R * a.C) return;
@@ -349,7 +353,11 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   const uint32_t i0s = (uint32_t)(a.begin + (uint64_t)wl * 32);  // < 2^32 when wl < wend
   // all 32 words of this lane are full and inside [begin, end)
   const bool full = (uint64_t)i0s + 1024 <= a.end && wl + 32 <= wend;
-  const bool extras = (r1 > r0) || a.rt.kind == AG_ROUTER_NOISY || (a.flags & AG_FORCE_TOP);
+  // noisy verdicts deferred to a warp-cooperative pass over the needed bits
+  // when the per-configuration hash is tabulated
+  const bool defer = a.rt.kind == AG_ROUTER_NOISY && a.hc != nullptr;
+  const bool extras = (r1 > r0) || (a.rt.kind == AG_ROUTER_NOISY && !defer) ||
+                      ((a.flags & AG_FORCE_TOP) && !defer);
   const bool pat = fast && !extras && a.pat_lg >= 0 && k <= kPatSeeds;
   if (pat) {
     // phase tables of this task's seeds: lanes own (seed, phase) entries
@@ -435,9 +443,9 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
           const uint64_t x = __ldg(a.t.removed + i);
           if (x >= i0 && x < i0 + nbits) word &= ~(1u << (uint32_t)(x - i0));
         }
-        if (a.rt.kind == AG_ROUTER_NOISY)
+        if (a.rt.kind == AG_ROUTER_NOISY && !defer)
           word = noisy_word<NT>(a.sp, (uint32_t)i0, nbits, word, a.rt, P);
-        if ((a.flags & AG_FORCE_TOP) && top >= i0 && top < i0 + nbits)
+        if ((a.flags & AG_FORCE_TOP) && !defer && top >= i0 && top < i0 + nbits)
           word |= 1u << (uint32_t)(top - i0);
         cnt += __popc(word);
       }
@@ -445,6 +453,73 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
     }
   }
   __syncwarp();
+  if (defer) {
+    // Noisy verdicts (router.cpp:50-57): key = mix({seed, 0xA3, id,
+    // hash_config(c)}) >> 11 = absorb(P, hc[c]) >> 11.  Per half group (16
+    // words = 512 configurations) the needed bits are listed bit-parallel
+    // (word it, lane j -> prefix + popc(need & lanemask_lt)), then every lane
+    // verdicts one listed configuration per pass and flips the bits the noise
+    // changes -- full lanes instead of one bit position per lane.
+    const uint32_t bit = 1u << lane, lt = bit - 1u;
+    uint16_t* lst = reinterpret_cast<uint16_t*>(&s_pat[wid]);
+    for (uint32_t h = 0; h < 64; ++h) {
+      const uint32_t L = h >> 1, it0 = (h & 1u) * 16;
+      const uint32_t wg = wbeg + 32 * L + it0;  // first word of the half group
+      if (wg >= wend) break;
+      const uint64_t ib = a.begin + (uint64_t)wg * 32;
+      // every word of the half group inside [begin, end): no tail masks
+      const bool hfull = wg + 16 <= wend && ib + 512 <= a.end;
+      const uint32_t keep_fn = (a.rt.t_fn > 0) ? 0xffffffffu : 0u, keep_fp = (a.rt.t_fp > 0) ? 0xffffffffu : 0u;
+      uint32_t n = 0;
+      for (uint32_t t = 0; t < 16; ++t) {
+        const uint32_t truth = s_tr[wid][L][it0 + t];
+        uint32_t valid = 0xffffffffu;
+        if (!hfull) {
+          const uint64_t i0 = ib + 32ull * t;
+          valid = (wg + t >= wend || i0 >= a.end) ? 0u
+                : (a.end - i0 >= 32 ? 0xffffffffu : ((1u << (uint32_t)(a.end - i0)) - 1u));
+        }
+        const uint32_t need = ((truth & keep_fn) | (~truth & keep_fp)) & valid;
+        if (need & bit) lst[n + __popc(need & lt)] = (uint16_t)(t * 32 + lane);
+        n += __popc(need);
+      }
+      __syncwarp();
+      // four listed configurations per lane per pass: the table loads of a
+      // pass are in flight together
+      for (uint32_t e0 = 0; e0 < n; e0 += 128) {
+        uint32_t off[4];
+        uint64_t hv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t e = e0 + 32 * u + lane;
+          off[u] = e < n ? lst[e] : 0xffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) hv[u] = off[u] != 0xffffu ? __ldg(a.hc + ib + off[u]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (off[u] == 0xffffu) continue;
+          const uint32_t t = off[u] >> 5, b = off[u] & 31u;
+          uint32_t* wp = &s_tr[wid][L][it0 + t];
+          const bool truth = (*wp >> b) & 1u;
+          const uint64_t key = absorb(P, hv[u]) >> 11;
+          const bool v = truth ? key >= a.rt.t_fn : key < a.rt.t_fp;
+          if (v != truth) atomicXor(wp, 1u << b);
+        }
+      }
+      __syncwarp();
+    }
+    if ((a.flags & AG_FORCE_TOP) && lane == 0) {
+      const uint64_t tb = a.begin + (uint64_t)wbeg * 32;
+      if (top >= tb && top < tb + 32ull * (wend - wbeg)) {
+        const uint32_t o = (uint32_t)(top - tb);
+        s_tr[wid][(o >> 5) >> 5][(o >> 5) & 31u] |= 1u << (o & 31u);
+      }
+    }
+    __syncwarp();
+    cnt = 0;
+    for (uint32_t it = 0; it < 32; ++it) cnt += __popc(s_tr[wid][lane][it]);
+  }
   uint32_t* brow = a.bitmap + (size_t)r * a.W + wbeg;
   const uint32_t nw = wend - wbeg;
   for (uint32_t it = 0; it < 32; ++it) {
@@ -708,6 +783,39 @@ score_fn pick_score(int n) {
 inline uint64_t magic_div(uint32_t d) { return d > 1 ? (~0ULL) / (uint64_t)d + 1 : 0; }
 
 // colmask[l0][c] = positions j in 0..31 with (l0 + j) mod M >= c
+// hash_config(c) (router.cpp:22-28) for every canonical index: the noisy
+// router's per-configuration state does not depend on the request, so it is
+// tabulated once per space (spaces up to kHashTableMax configurations).
+constexpr uint64_t kHashTableMax = 1ull << 24;
+
+__global__ void k_hash_table(SpaceDev sp, uint64_t* __restrict__ hc) {
+  const uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= sp.size) return;
+  uint32_t d[kMaxAgents];
+  uint32_t x = (uint32_t)c;
+  for (int a = sp.n - 1; a >= 0; --a) {
+    const uint32_t q = divm(x, sp.div_m);
+    d[a] = x - q * (uint32_t)sp.m;
+    x = q;
+  }
+  uint64_t h = kHashIV;
+  for (int a = 0; a < sp.n; ++a) h = absorb(absorb(kMixIV, h), d[a]);  // mix({h, m})
+  hc[c] = h;
+}
+
+const uint64_t* ensure_hash_table(ag_ctx* ctx) {
+  const ag_space* sp = ctx->space;
+  if (sp->size > kHashTableMax) return nullptr;
+  if (!ctx->hc_ready) {
+    if (ctx->hc.ensure(8 * sp->size + 8)) return nullptr;
+    const unsigned blocks = (unsigned)((sp->size + 255) / 256);
+    k_hash_table<<<blocks, 256, 0, ctx->stream>>>(sp->dev(), (uint64_t*)ctx->hc.p);
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+    ctx->hc_ready = true;
+  }
+  return (const uint64_t*)ctx->hc.p;
+}
+
 int ensure_colmask(ag_ctx* ctx) {
   const int m = ctx->space->m;
   if (ctx->colmask.bytes >= 32 * 32 * 4 && ctx->colmask_m == m) return AG_OK;
@@ -833,6 +941,7 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
     a.pat_lg = (a.path2d && Bq >= 32 && a.pat_P <= kPatMax) ? __builtin_ctz(g) : -1;
   }
   a.colmask = (const uint32_t*)ctx->colmask.p;
+  a.hc = rt.kind == AG_ROUTER_NOISY ? ensure_hash_table(ctx) : nullptr;
   a.bitmap = bitmap;
   a.task_counts = (uint32_t*)ctx->chunk_counts.p;
   const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
