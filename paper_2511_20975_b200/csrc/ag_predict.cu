@@ -335,7 +335,12 @@ struct ag_predictor {
   uint32_t uid_top = 0;
   std::vector<uint64_t> chains_host;  // canonical indices [n_chains * len]
   agb::Scratch d_chain_uid, d_uniq_index, d_by_cost, d_by_index, d_scratch;
-  agb::Scratch d_out;  // ag_predict_host outputs
+  void* h_out = nullptr;  // ag_predict_host outputs, mapped pinned memory
+  size_t h_out_bytes = 0;
+  char* h_out_dev = nullptr;
+  ~ag_predictor() {
+    if (h_out) cudaFreeHost(h_out);
+  }
 };
 
 using agb::fail;
@@ -499,21 +504,37 @@ int ag_predict_host(ag_predictor* p, const ag_truth* th, const ag_router* router
   const size_t o_t = (o_f + 4 * (size_t)R + 7) & ~(size_t)7;
   const size_t o_b = o_t + 8 * (size_t)R, o_u = o_b + 8 * (size_t)R;
   const size_t bytes = o_u + (size_t)R;
-  if ((rc = p->d_out.ensure(bytes))) return rc;
-  char* d = (char*)p->d_out.p;
+  // outputs (and budgets) in mapped pinned memory: the kernel writes the
+  // host's copy directly, one launch + one synchronisation per call
+  if (bytes > p->h_out_bytes) {
+    if (p->h_out) cudaFreeHost(p->h_out);
+    p->h_out = nullptr;
+    p->h_out_bytes = 0;
+    AG_CUDA(cudaHostAlloc(&p->h_out, std::max<size_t>(bytes, 4096), cudaHostAllocMapped));
+    p->h_out_bytes = std::max<size_t>(bytes, 4096);
+    void* dv = nullptr;
+    AG_CUDA(cudaHostGetDevicePointer(&dv, p->h_out, 0));
+    p->h_out_dev = (char*)dv;
+  }
+  char* hbuf = (char*)p->h_out;
+  char* d = p->h_out_dev;
   cudaStream_t s = ctx->stream;
-  if (budgets) AG_CUDA(cudaMemcpyAsync(d + o_b, budgets, 8 * (size_t)R, cudaMemcpyHostToDevice, s));
+  if (budgets) std::memcpy(hbuf + o_b, budgets, 8 * (size_t)R);
   ag_predict_out o{(uint32_t*)(d + o_v), viable_stride, (int32_t*)(d + o_n), (int32_t*)(d + o_s),
                    (int32_t*)(d + o_f), (double*)(d + o_t), (uint8_t*)(d + o_u)};
   if ((rc = ag_predict(p, &td, router, budgets ? (const double*)(d + o_b) : nullptr, budget_all, &o)))
     return rc;
-  AG_CUDA(cudaMemcpyAsync(n_viable, d + o_n, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
-  AG_CUDA(cudaMemcpyAsync(viable, d + o_v, 4 * (size_t)R * viable_stride, cudaMemcpyDeviceToHost, s));
-  if (search_evals) AG_CUDA(cudaMemcpyAsync(search_evals, d + o_s, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
-  if (verify_evals) AG_CUDA(cudaMemcpyAsync(verify_evals, d + o_f, 4 * (size_t)R, cudaMemcpyDeviceToHost, s));
-  if (router_time) AG_CUDA(cudaMemcpyAsync(router_time, d + o_t, 8 * (size_t)R, cudaMemcpyDeviceToHost, s));
-  if (truncated) AG_CUDA(cudaMemcpyAsync(truncated, d + o_u, (size_t)R, cudaMemcpyDeviceToHost, s));
   AG_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(n_viable, hbuf + o_n, 4 * (size_t)R);
+  for (int r = 0; r < R; ++r) {  // only each request's viable prefix is meaningful
+    const int32_t nv = ((const int32_t*)(hbuf + o_n))[r];
+    std::memcpy(viable + (size_t)r * viable_stride, hbuf + o_v + 4 * (size_t)r * viable_stride,
+                4 * (size_t)std::max(0, std::min(nv, viable_stride)));
+  }
+  if (search_evals) std::memcpy(search_evals, hbuf + o_s, 4 * (size_t)R);
+  if (verify_evals) std::memcpy(verify_evals, hbuf + o_f, 4 * (size_t)R);
+  if (router_time) std::memcpy(router_time, hbuf + o_t, 8 * (size_t)R);
+  if (truncated) std::memcpy(truncated, hbuf + o_u, (size_t)R);
   return AG_OK;
 }
 

@@ -1338,6 +1338,8 @@ struct ag_sched {
   void* h_res_mapped = nullptr;
   char* h_rstage_dev = nullptr;
   int32_t* h_res_dev = nullptr;
+  void* h_vstage = nullptr;  // viable lists of added requests
+  size_t h_vstage_bytes = 0;
   void* h_ostage = nullptr;  // FIFO re-uploads after a compaction
   size_t h_ostage_bytes = 0;
   ~ag_sched() {
@@ -1345,6 +1347,7 @@ struct ag_sched {
     if (h_stage) cudaFreeHost(h_stage);
     if (h_rstage) cudaFreeHost(h_rstage);
     if (h_ostage) cudaFreeHost(h_ostage);
+    if (h_vstage) cudaFreeHost(h_vstage);
   }
 };
 
@@ -1788,8 +1791,15 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
     agb::set_ready(s, slot, agb::ready_of(s, slot));
     if (slots_out) slots_out[i] = slot;
   }
-  AG_CUDA(cudaMemcpyAsync((uint32_t*)s->d_pool.p + s->pool_top, q->viable + q->viable_ptr[0],
-                          total * 4, cudaMemcpyHostToDevice, ctx->stream));
+  {
+    // through pinned staging: a pageable source would make the copy synchronous
+    AG_CUDA(cudaStreamSynchronize(ctx->stream));  // the staging buffer's previous copy
+    int rc0 = agb::ensure_pinned(&s->h_vstage, &s->h_vstage_bytes, total * 4 + 4);
+    if (rc0) return rc0;
+    std::memcpy(s->h_vstage, q->viable + q->viable_ptr[0], total * 4);
+    AG_CUDA(cudaMemcpyAsync((uint32_t*)s->d_pool.p + s->pool_top, s->h_vstage, total * 4,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  }
   s->pool_top += total;
   // FIFO insertion (Sim::insert_schedulable, simulation.cpp:182-192)
   for (int i = 0; i < R; ++i) {
