@@ -146,15 +146,44 @@ def ref_sched(rounds):
     return json.loads(out.strip().splitlines()[-1])
 
 
+def host_info():
+    """CPU model, cores, compiler of the reference build."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        gxx = subprocess.run(["g++", "--version"], capture_output=True, text=True).stdout.splitlines()[0]
+    except (OSError, IndexError):
+        gxx = "unknown"
+    return {"cpu": model, "nproc": os.cpu_count(), "compiler": gxx,
+            "flags": "-std=c++20 -O2 (no -march: no FMA contraction, as the reference)"}
+
+
 def cpu_baseline(sample=CPU_SAMPLE_REQUESTS, threads=None):
-    """The reference's own enumerate-mode loop on the host cores (ref_bench)."""
+    """The reference's own enumerate-mode loop on the host cores (ref_bench),
+    plus one core, the chain-mode predictor and the host description."""
     threads = threads or os.cpu_count()
     if os.path.exists(REF_BENCH):
         r = ref_route(sample, threads)
+        one = ref_route(max(sample // 10, 1), 1)
+        out = subprocess.run([REF_BENCH, "predict", str(N_AGENTS), str(N_TIERS), "2000", "oracle",
+                              str(threads), str(SEED)], capture_output=True, text=True,
+                             check=True).stdout
+        pr = json.loads(out.strip().splitlines()[-1])
         return {"value": r["configs_per_s"], "unit": UNIT, "cores": threads, "kind": "reference",
                 "sample": f"first {sample} requests of config 2 "
                           f"({sample * N_TIERS ** N_AGENTS:.3g} configs), reference "
-                          "at_index+OracleRouter::evaluate loop under parallel_for"}
+                          "at_index+OracleRouter::evaluate loop under parallel_for",
+                "one_core": {"value": one["configs_per_s"], "unit": UNIT,
+                             "sample": f"{max(sample // 10, 1)} requests"},
+                "chain_mode": {"value": pr["requests_per_s"], "unit": "requests/s",
+                               "cores": threads, "sample": "2000 requests, predict(inf)"},
+                "host": host_info()}
     # port: the C restatement, single thread, bounded sample
     from oracle import oracle as O
     import paper_2511_20975_b200 as P
@@ -413,6 +442,31 @@ def run_ours(args):
     e2e_ok = int(hb_offsets[-1]) == total_members
     P.lib().ag_host_free(pinned)
 
+    # chain mode (ConfigPredictor::predict, the reference's routing call):
+    # the same 10k requests, unbounded budget and the 0.002 s evaluation charge
+    chain = None
+    if not args.no_chain:
+        pred = P.ConfigPredictor(dev)
+        crouter = P.OracleRouter(0.002)
+        for _ in range(2):
+            pred.predict_batch(truth, crouter)
+        cev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(5)]
+        barrier()
+        for i in range(5):
+            flush.fill_(i & 0xFF)
+            cev[i][0].record(stream)
+            cres = pred.predict_batch(truth, crouter)
+            cev[i][1].record(stream)
+        barrier()
+        cms = statistics.median([x.elapsed_time(y) for x, y in cev])
+        chain = {"workload": "config2 requests through ConfigPredictor::predict (chain plan, "
+                             "binary search, verification; budget inf)",
+                 "requests_per_s": REQUESTS_PER_GPU / (cms / 1e3), "ms_per_batch": cms,
+                 "evaluations_per_request": float((cres.search_evals + cres.verify_evals)
+                                                  .double().mean().item()),
+                 "viable_per_request": float(cres.n_viable.double().mean().item())}
+        del pred, cres
     # the same batch with the noisy router of BASELINE config 2 (fp 0, fn 0.3,
     # seed 7): integer-issue bound (two splitmix64 per needed configuration)
     noisy = None
@@ -487,6 +541,7 @@ def run_ours(args):
         "sched": sched,
         "deep": deep,
         "noisy": noisy,
+        "chain": chain,
         "config5": config5,
         "clocks": clk,
     }
@@ -510,6 +565,7 @@ def main():
     ap.add_argument("--no-deep", action="store_true")
     ap.add_argument("--no-config5", action="store_true")
     ap.add_argument("--no-noisy", action="store_true")
+    ap.add_argument("--no-chain", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
