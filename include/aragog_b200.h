@@ -80,7 +80,7 @@ uint64_t ag_ctx_launch_count(const ag_ctx* ctx);
  * events on the context stream.  ag_ctx_profile_end synchronises the stream
  * and returns, per kernel id (0 .. AG_NUM_KERNELS-1), the summed device
  * milliseconds and launch counts since ag_ctx_profile_begin. */
-#define AG_NUM_KERNELS 9
+#define AG_NUM_KERNELS 10
 int ag_ctx_profile_begin(ag_ctx* ctx);
 int ag_ctx_profile_end(ag_ctx* ctx, double* ms, uint64_t* launches);
 const char* ag_kernel_name(int kernel_id);
@@ -157,6 +157,27 @@ int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* truth_host,
                             uint64_t end, uint32_t flags, uint64_t* counts,
                             uint64_t* offsets, uint32_t* indices,
                             uint64_t capacity, uint64_t* total);
+
+/* ---- learned router ----------------------------- */
+/* The paper's fused classifier heads as a RouterBackend: one linear head per
+ * canonical configuration, verdict(r, c) = emb[r] . heads[c] + bias[c] > 0.
+ * Not in the reference: parity is against the numpy restatement in oracle/
+ * within fp32 accumulation tolerance.  Device pointers; heads / emb rows of
+ * `dim` bf16 (dim a multiple of 16, <= 128, rows 16-byte aligned), indexed by
+ * canonical configuration index / request row; bias fp32 [size]. */
+typedef struct {
+  int32_t dim;
+  const void* heads; /* bf16 [space size][dim] */
+  const float* bias; /* [space size] */
+} ag_linear_heads;
+
+/* Enumerate mode with the learned router: scores every configuration in
+ * [begin, end) of every request as the tcgen05 contraction emb . heads^T
+ * with a fused threshold epilogue into the verdict bitmap, then the same
+ * scans and compaction as ag_route_enumerate (out as there). */
+int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
+                    const ag_linear_heads* heads, uint64_t begin, uint64_t end,
+                    uint32_t flags, const ag_route_out* out_dev);
 
 /* ---- chain mode ---------------------------------------------------------- */
 typedef struct ag_predictor ag_predictor;

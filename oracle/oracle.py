@@ -341,3 +341,10 @@ def prefix_prune(n, m, viable, agent, model):
     v = np.ascontiguousarray(viable, np.uint64).copy()
     k = _lib().ago_prefix_prune(n, m, C.c_void_p(_p(v)), len(v), agent, model)
     return None if k < 0 else v[:k]
+
+
+def linear_logits(emb, heads, bias):
+    """The learned router of SURVEY.md §8(f) rank 3 (not in the reference):
+    logit(r, c) = emb[r] . heads[c] + bias[c], verdict = logit > 0, in fp64
+    from the bf16 inputs (given as float arrays).  Test infrastructure only."""
+    return np.asarray(emb, np.float64) @ np.asarray(heads, np.float64).T + np.asarray(bias, np.float64)[None, :]

@@ -50,12 +50,26 @@ class RouteOut(C.Structure):
                 ("indices", C.c_void_p), ("capacity", C.c_uint64), ("overflow", C.c_void_p)]
 
 
+class LinearHeads(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("heads", C.c_void_p), ("bias", C.c_void_p)]
+
+
 class GenParams(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("p_easy", "p_medium", "p_hard", "easy_base_prob",
                                            "violation_rate")]
 
 
 _lib = None
+
+
+def release(fn_name: str, handle) -> None:
+    """Destroy a C handle from __del__; a no-op during interpreter shutdown
+    (module globals already torn down) or when the library never loaded."""
+    try:
+        if _lib is not None and handle is not None and handle.value:
+            getattr(_lib, fn_name)(handle)
+    except Exception:  # noqa: BLE001 -- finalizers must not raise
+        pass
 
 
 def lib() -> C.CDLL:

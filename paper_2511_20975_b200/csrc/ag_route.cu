@@ -946,29 +946,41 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   a.task_counts = (uint32_t*)ctx->chunk_counts.p;
   const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
   if (range > 0) {
-    {
-      Launch L(ctx, K_ROUTE_SCORE);
-      pick_score(sp->n)(grid, s, a);
-    }
-    {
-      Launch L(ctx, K_CHUNK_SCAN);
-      if (C * 32 <= 4096)
-        k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
-            (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
-      else
-        k_chunk_scan_block<<<R, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
-                                              (uint64_t*)ctx->chunk_off.p, out->counts, C * 32);
-    }
+    Launch L(ctx, K_ROUTE_SCORE);
+    pick_score(sp->n)(grid, s, a);
   } else {
     AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
+    Launch L(ctx, K_REQUEST_SCAN);
+    k_request_scan<<<1, 1024, 0, s>>>(out->counts, offsets, R,
+                                     out->indices ? out->capacity : ~0ULL, out->overflow);
+    AG_CUDA(cudaGetLastError());
+    return AG_OK;
+  }
+  return finish_enumerate(ctx, R, W, C, begin, bitmap, offsets, out);
+}
+
+// K2 scans + K3 compaction of a verdict bitmap [R][W] whose per-group counts
+// ([R][C*32], 32-word groups) are in ctx->chunk_counts: shared by the oracle /
+// noisy scoring kernel and the learned router (ag_linear.cu).
+int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, uint32_t* bitmap,
+                     uint64_t* offsets, const ag_route_out* out) {
+  cudaStream_t s = ctx->stream;
+  {
+    Launch L(ctx, K_CHUNK_SCAN);
+    if (C * 32 <= 4096)
+      k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
+          (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
+    else
+      k_chunk_scan_block<<<R, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
+                                            (uint64_t*)ctx->chunk_off.p, out->counts, C * 32);
   }
   {
     Launch L(ctx, K_REQUEST_SCAN);
     k_request_scan<<<1, 1024, 0, s>>>(out->counts, offsets, R,
                                      out->indices ? out->capacity : ~0ULL, out->overflow);
   }
-  if (out->indices && range > 0) {
-    rc = launch_compact(ctx, R, W, C, begin, bitmap, offsets, out->indices, out->capacity);
+  if (out->indices) {
+    const int rc = launch_compact(ctx, R, W, C, begin, bitmap, offsets, out->indices, out->capacity);
     if (rc) return rc;
   }
   AG_CUDA(cudaGetLastError());

@@ -86,7 +86,5 @@ class ConfigPredictor:
         return res
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().ag_predictor_destroy(h)
-            self._h = None
+        _capi.release("ag_predictor_destroy", getattr(self, "_h", None))
+        self._h = None

@@ -84,10 +84,8 @@ class ConfigSpace:
         return self.size - 1
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().ag_space_destroy(h)
-            self._h = None
+        _capi.release("ag_space_destroy", getattr(self, "_h", None))
+        self._h = None
 
 
 @dataclass
@@ -255,7 +253,7 @@ class Device:
 
     def profile_end(self) -> dict:
         """{kernel name: (total device ms, launches)} since profile_begin."""
-        k = 9
+        k = 10  # AG_NUM_KERNELS
         ms = (C.c_double * k)()
         n = (C.c_uint64 * k)()
         check(lib().ag_ctx_profile_end(self._h, ms, n))
@@ -298,6 +296,29 @@ class Device:
         self._last_out = out
         return RouteResult(out["counts"], out["offsets"], out["indices"], out["bitmap"])
 
+    def route_linear(self, emb, heads, bias, begin=0, end=None, force_top=False, out=None,
+                     capacity=None, bitmap=False) -> RouteResult:
+        """Enumerate mode with the learned router (ag_route_linear): device
+        tensors emb [R, D] bf16, heads [space size, D] bf16, bias [size] f32;
+        verdict = emb . heads[c] + bias[c] > 0 (async on the context stream)."""
+        import torch
+
+        end = self.space.size if end is None else end
+        R = int(emb.shape[0])
+        if out is None:
+            out = self.alloc_route(R, begin, end, R * (end - begin) if capacity is None else capacity,
+                                   bitmap)
+        assert emb.dtype == torch.bfloat16 and heads.dtype == torch.bfloat16
+        assert bias.dtype == torch.float32
+        lh = _capi.LinearHeads(int(heads.shape[1]), _ptr(heads), _ptr(bias))
+        ro = _capi.RouteOut(_ptr(out["bitmap"]), _ptr(out["counts"]), _ptr(out["offsets"]),
+                            _ptr(out["indices"]), out["capacity"], _ptr(out["overflow"]))
+        check(lib().ag_route_linear(self._h, C.c_void_p(_ptr(emb)), R, C.byref(lh), C.c_uint64(begin),
+                                    C.c_uint64(end),
+                                    C.c_uint32(_capi.AG_FORCE_TOP if force_top else 0), C.byref(ro)))
+        self._last_out = (out, emb, heads, bias)
+        return RouteResult(out["counts"], out["offsets"], out["indices"], out["bitmap"])
+
     def route_enumerate_host(self, truth: AccuracyBatch, router, begin=0, end=None,
                              force_top=False, capacity=None, indices=None, counts=None,
                              offsets=None):
@@ -319,10 +340,8 @@ class Device:
         return RouteResult(counts, offsets, indices[: total.value], None)
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().ag_ctx_destroy(h)
-            self._h = None
+        _capi.release("ag_ctx_destroy", getattr(self, "_h", None))
+        self._h = None
 
 
 def enumerate_members(space: ConfigSpace, seeds, removed=(), device: Device | None = None):

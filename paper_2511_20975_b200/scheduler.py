@@ -12,6 +12,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from . import _capi
 from ._capi import check, lib
 from .routing import Device, _ptr
 
@@ -179,10 +180,8 @@ class SchedSession:
         return out[: n.value]
 
     def __del__(self):
-        h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            lib().ag_sched_destroy(h)
-            self._h = None
+        _capi.release("ag_sched_destroy", getattr(self, "_h", None))
+        self._h = None
 
 
 class CLoad(C.Structure):
