@@ -467,6 +467,51 @@ def run_ours(args):
                                                   .double().mean().item()),
                  "viable_per_request": float(cres.n_viable.double().mean().item())}
         del pred, cres
+    # the learned router: per-configuration linear
+    # heads, the contraction emb . heads^T on tcgen05 with the threshold fused
+    # into the epilogue; synthetic bf16 embeddings / heads (no reference)
+    linear = None
+    if not args.no_linear:
+        D = 128
+        gl = torch.Generator(device=dev_t).manual_seed(SEED)
+        emb = torch.randn(REQUESTS_PER_GPU, D, device=dev_t, generator=gl).to(torch.bfloat16)
+        heads = (torch.randn(S, D, device=dev_t, generator=gl) / D ** 0.5).to(torch.bfloat16)
+        lbias = torch.randn(S, device=dev_t, generator=gl) * 0.1 - 0.2
+        lprobe = dev.route_linear(emb, heads, lbias, capacity=1)
+        torch.cuda.synchronize()
+        lmem = int(lprobe.offsets[-1])
+        lout = dev.alloc_route(REQUESTS_PER_GPU, 0, S, lmem)
+        for _ in range(3):
+            dev.route_linear(emb, heads, lbias, out=lout)
+        lev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(5)]
+        barrier()
+        dev.profile_begin()
+        for i in range(5):
+            flush.fill_(i & 0xFF)
+            lev[i][0].record(stream)
+            dev.route_linear(emb, heads, lbias, out=lout)
+            lev[i][1].record(stream)
+        lprof = dev.profile_end()
+        barrier()
+        lms = statistics.median([x.elapsed_time(y) for x, y in lev])
+        kms = lprof["k_linear_score"][0] / lprof["k_linear_score"][1]
+        flops = 2.0 * REQUESTS_PER_GPU * S * D
+        try:
+            pk = json.load(open(PEAKS))["bf16_tflops"]
+            pks = "measured burst bf16 (MEASURED_PEAKS.json)"
+        except (OSError, KeyError, ValueError):
+            pk, pks = 1590.0, "fallback (B200_PROFILING.md)"
+        linear = {"router": f"linear heads, D {D}, bf16 -> fp32 (tcgen05 kind::f16, M128 N256)",
+                  "configs_per_s": REQUESTS_PER_GPU * S / (lms / 1e3), "ms_per_step": lms,
+                  "members_per_step": lmem,
+                  "kernel_ms": {k: v[0] / v[1] for k, v in lprof.items()},
+                  "roofline": {"bound": "tensor", "kernel": "k_linear_score",
+                               "achieved": flops / (kms / 1e3) / 1e12, "peak": pk,
+                               "unit": "TFLOP/s", "frac": flops / (kms / 1e3) / 1e12 / pk,
+                               "peak_source": pks},
+                  "note": "epilogue-bound: one threshold per output bit against 2*D = 256 flops"}
+        del lout, lprobe, emb, heads, lbias
     # the same batch with the noisy router of BASELINE config 2 (fp 0, fn 0.3,
     # seed 7): integer-issue bound (two splitmix64 per needed configuration)
     noisy = None
@@ -541,6 +586,7 @@ def run_ours(args):
         "sched": sched,
         "deep": deep,
         "noisy": noisy,
+        "linear": linear,
         "chain": chain,
         "config5": config5,
         "clocks": clk,
@@ -566,6 +612,7 @@ def main():
     ap.add_argument("--no-config5", action="store_true")
     ap.add_argument("--no-noisy", action="store_true")
     ap.add_argument("--no-chain", action="store_true")
+    ap.add_argument("--no-linear", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -15,10 +15,10 @@
 //     layout (8-row x 16-byte core matrices, K-chunks 128 B apart); one thread
 //     issues tcgen05.mma kind::f16 (M 128, N 256, K 16) into a TMEM
 //     accumulator (two 256-column buffers) and commits to an mbarrier;
-//   * the epilogue warps (TMEM lane quarters 0-3) read 32 accumulator columns
-//     at a time with tcgen05.ld, threshold against the row's bias, and one
-//     warp ballot per column turns 32 configurations into the request's
-//     bitmap word -- the verdict bitmap comes out in the same [R][W] layout
+//   * the epilogue warps (4 per TMEM lane quarter) read 32 accumulator
+//     columns at a time with tcgen05.ld, threshold against the row's bias
+//     into a 32-bit row mask, and a 32x32 bit transpose across the warp turns
+//     32 configurations into each request's bitmap word -- the verdict bitmap comes out in the same [R][W] layout
 //     as k_route_score, so the scans and k_route_compact finish the job.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,8 +32,10 @@ namespace {
 
 constexpr int kLinM = 128;        // configurations per MMA tile
 constexpr int kLinN = 256;        // requests per CTA
-constexpr int kLinTiles = 8;      // configuration tiles per CTA (1024 configs)
-constexpr int kLinThreads = 256;  // warps 0-3 epilogue, 4-7 loaders (+ MMA issue)
+constexpr int kLinTiles = 16;     // configuration tiles per CTA (2 groups of 1024)
+constexpr int kEpiWarps = 16;     // epilogue: 4 per TMEM lane quarter, 64 columns each
+constexpr int kLdWarps = 4;       // cp.async loaders
+constexpr int kLinThreads = 32 * (kEpiWarps + kLdWarps + 1);  // + the MMA issuer
 constexpr int kWbStride = 33;     // padded words per request row
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -49,112 +51,154 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1 (sm100)
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t phase) {
+__device__ __forceinline__ void mbar_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(mb)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* mb) {
+  asm volatile("{ .reg .b64 st; mbarrier.arrive.shared::cta.b64 st, [%0]; }" ::"r"(su32(mb)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
   uint32_t done = 0;
   while (!done)
     asm volatile(
         "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
         : "=r"(done)
-        : "r"(su32(mb)), "r"(phase)
+        : "r"(su32(mb)), "r"(parity)
         : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* mb) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mb))
+               : "memory");
+}
+// 16-byte async copy global -> shared (zero-filled when !valid)
+__device__ __forceinline__ void cp16(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
 }
 
 struct LinArgs {
-  const uint4* emb;     // [R][D] bf16, 16-byte rows chunks
+  const uint4* emb;     // [R][D] bf16, 16-byte row chunks
   const uint4* heads;   // [S][D] bf16 (indexed by canonical index)
   const float* bias;    // [S]
   int R, D;
   uint64_t begin, end, top;
   uint32_t W, C;        // words per request, tasks (of 32 groups) per request
+  uint32_t G;           // 32-word groups per request
   uint32_t flags;
   uint32_t* bitmap;     // [R][W]
   uint32_t* task_counts;  // [R][C*32] popcount per 32-word group
 };
 
+// Warp-specialised: the loaders keep two A stages ahead (cp.async), the
+// issuer runs the tensor core into two TMEM buffers, the epilogue drains one
+// buffer while the other fills; full/empty mbarriers for both hand-offs.
 __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int KC = a.D / 8;                        // 16-byte K-chunks per row
   unsigned char* sb = smem;                      // [256 requests][D] core-matrix layout
-  unsigned char* sa0 = sb + (size_t)kLinN * a.D * 2;
-  unsigned char* sa1 = sa0 + (size_t)kLinM * a.D * 2;
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sa1 + (size_t)kLinM * a.D * 2);  // [256][33]
+  unsigned char* sa[2];
+  sa[0] = sb + (size_t)kLinN * a.D * 2;
+  sa[1] = sa[0] + (size_t)kLinM * a.D * 2;
+  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sa[1] + (size_t)kLinM * a.D * 2);  // [256][33]
   __shared__ uint32_t s_tmem;
-  __shared__ __align__(8) uint64_t s_mbar[2];
+  __shared__ __align__(8) uint64_t b_full, a_full[2], a_empty[2], t_full[2], t_empty[2];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int rt = blockIdx.y;                      // request tile
-  const uint32_t g = blockIdx.x;                  // 1024-configuration group
-  const uint64_t cbase = a.begin + (uint64_t)g * (kLinM * kLinTiles);
-  const int r0 = rt * kLinN;
+  const int r0 = blockIdx.y * kLinN;
+  const uint64_t cbase = a.begin + (uint64_t)blockIdx.x * (kLinM * kLinTiles);
+  // tiles of this CTA that hold any configuration of [begin, end)
+  const int T = (int)min((uint64_t)kLinTiles, (a.end - cbase + kLinM - 1) / kLinM);
 
   if (wid == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_mbar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&s_mbar[1])));
-  }
-  // loaders: a configuration tile of heads into a core-matrix buffer
-  auto load_a = [&](int t, unsigned char* sa) {
-    const uint64_t c0 = cbase + (uint64_t)t * kLinM;
-    for (int i = tid - 128; i < kLinM * KC; i += 128) {
-      const int row = i / KC, kc = i - row * KC;
-      const uint64_t c = c0 + row;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (c < a.end) v = __ldg(a.heads + c * KC + kc);
-      *reinterpret_cast<uint4*>(sa + cm_off(row, kc, KC)) = v;
+    mbar_init(&b_full, 32 * kLdWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&a_full[i], 32 * kLdWarps);
+      mbar_init(&a_empty[i], 1);
+      mbar_init(&t_full[i], 1);
+      mbar_init(&t_empty[i], 32 * kEpiWarps);
     }
-  };
-  if (wid >= 4) {
-    for (int i = tid - 128; i < kLinN * KC; i += 128) {
-      const int row = i / KC, kc = i - row * KC;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (r0 + row < a.R) v = __ldg(a.emb + (size_t)(r0 + row) * KC + kc);
-      *reinterpret_cast<uint4*>(sb + cm_off(row, kc, KC)) = v;
-    }
-    load_a(0, sa0);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core proxy
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  // instruction descriptor: bf16 x bf16 -> f32, K-major both, M 128, N 256
-  const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLinN >> 3) << 17) |
-                         ((uint32_t)(kLinM >> 4) << 24);
-  const uint32_t lbo = 128, sbo = (uint32_t)KC * 128;
-  auto issue = [&](int t) {
-    const unsigned char* sa = (t & 1) ? sa1 : sa0;
-    const uint32_t acc_col = tmem + (uint32_t)((t & 1) * kLinN);
-    for (int ks = 0; ks < a.D / 16; ++ks) {
-      const uint64_t da = sdesc(su32(sa) + ks * 256, lbo, sbo);
-      const uint64_t db = sdesc(su32(sb) + ks * 256, lbo, sbo);
-      const uint32_t accumulate = ks > 0 ? 1u : 0u;
-      asm volatile(
-          "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-          "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc_col),
-          "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
-          : "memory");
+
+  constexpr int kLd = 32 * kLdWarps;
+  if (wid >= kEpiWarps && wid < kEpiWarps + kLdWarps) {
+    // ---------------------------------------------------------- loaders
+    const int lt = tid - 32 * kEpiWarps;
+    for (int i = lt; i < kLinN * KC; i += kLd) {
+      const int row = i / KC, kc = i - row * KC;
+      const bool ok = r0 + row < a.R;
+      cp16(sb + cm_off(row, kc, KC), a.emb + (size_t)(ok ? r0 + row : 0) * KC + kc, ok);
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     su32(&s_mbar[t & 1]))
-                 : "memory");
-  };
-  if (tid == 128) issue(0);
-  for (int t = 0; t < kLinTiles; ++t) {
-    if (wid >= 4) {
-      if (t + 1 < kLinTiles) load_a(t + 1, ((t + 1) & 1) ? sa1 : sa0);
-    } else {
-      // epilogue: rows = configurations (lane = configuration within the
-      // warp's 32), columns = requests
-      mbar_wait(&s_mbar[t & 1], (uint32_t)((t >> 1) & 1));
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive(&b_full);
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1;
+      mbar_wait(&a_empty[s], ((t >> 1) & 1) ^ 1);
+      const uint64_t c0 = cbase + (uint64_t)t * kLinM;
+      for (int i = lt; i < kLinM * KC; i += kLd) {
+        const int row = i / KC, kc = i - row * KC;
+        const uint64_t c = c0 + row;
+        const bool ok = c < a.end;
+        cp16(sa[s] + cm_off(row, kc, KC), a.heads + (ok ? c : 0) * KC + kc, ok);
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&a_full[s]);
+    }
+  } else if (wid == kEpiWarps + kLdWarps) {
+    // ---------------------------------------------------------- MMA issue
+    if (lane == 0) {
+      // bf16 x bf16 -> f32, K-major both, M 128, N 256
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLinN >> 3) << 17) |
+                             ((uint32_t)(kLinM >> 4) << 24);
+      const uint32_t lbo = 128, sbo = (uint32_t)KC * 128;
+      mbar_wait(&b_full, 0);
+      for (int t = 0; t < T; ++t) {
+        const int s = t & 1;
+        mbar_wait(&a_full[s], (t >> 1) & 1);
+        mbar_wait(&t_empty[s], ((t >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(s * kLinN);
+        for (int ks = 0; ks < a.D / 16; ++ks) {
+          const uint64_t da = sdesc(su32(sa[s]) + ks * 256, lbo, sbo);
+          const uint64_t db = sdesc(su32(sb) + ks * 256, lbo, sbo);
+          const uint32_t accumulate = ks > 0 ? 1u : 0u;
+          asm volatile(
+              "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
+              "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+              : "memory");
+        }
+        umma_commit(&a_empty[s]);  // stage s may be refilled once these MMAs are done
+        umma_commit(&t_full[s]);   // and the accumulator is ready
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    // rows = configurations (lane = configuration in the warp's 32; warp w
+    // reads TMEM lane quarter w % 4), columns = requests (warp w takes the
+    // 64 columns (w / 4) * 64 ..); one ballot per column gives a word
+    const int q = wid & 3, h = wid >> 2;
+    constexpr int kCols = kLinN / (kEpiWarps / 4);
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1;
+      mbar_wait(&t_full[s], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t c = cbase + (uint64_t)t * kLinM + (uint64_t)(wid * 32 + lane);
+      const uint64_t c = cbase + (uint64_t)t * kLinM + (uint64_t)(q * 32 + lane);
       const float thr = c < a.end ? -__ldg(a.bias + c) : INFINITY;  // acc + b > 0 <=> acc > -b
-      const int widx = t * 4 + wid;  // word of the group
-      for (int c0 = 0; c0 < kLinN; c0 += 32) {
+      const int widx = (t & 7) * 4 + q;  // word within the group
+      for (int c0 = h * kCols; c0 < (h + 1) * kCols; c0 += 32) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(wid * 32) << 16) + (uint32_t)((t & 1) * kLinN + c0);
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * kLinN + c0);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -165,37 +209,49 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
               "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        uint32_t mine = 0;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const uint32_t w = __ballot_sync(0xffffffffu, __uint_as_float(v[j]) > thr);
-          if (lane == j) mine = w;
+        if (c0 + 32 == (h + 1) * kCols) {  // this warp's part is drained
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          mbar_arrive(&t_empty[s]);
         }
-        wbuf[(c0 + lane) * kWbStride + widx] = mine;
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (tid == 128 && t + 1 < kLinTiles) issue(t + 1);
-  }
-  // write the group: request rows of 32 words, top forced, tail masked
-  const uint64_t wfirst = (uint64_t)g * 32;  // first word of the group
-  for (int rr = wid; rr < kLinN; rr += kLinThreads / 32) {
-    const int r = r0 + rr;
-    if (r >= a.R) break;
-    const uint64_t wi = wfirst + lane;
-    uint32_t w = wbuf[rr * kWbStride + lane];
-    const uint64_t i0 = a.begin + wi * 32;
-    if (wi >= a.W) w = 0;
-    else if (a.end - i0 < 32) w &= (1u << (uint32_t)(a.end - i0)) - 1u;
-    if ((a.flags & AG_FORCE_TOP) && a.top >= i0 && a.top < i0 + 32 && wi < a.W) w |= 1u << (uint32_t)(a.top - i0);
-    if (wi < a.W) a.bitmap[(size_t)r * a.W + wi] = w;
-    uint32_t cnt = __popc(w);
+        // lane = configuration row: bit j = verdict for request column j;
+        // a 32x32 bit transpose across the warp turns rows into the
+        // requests' words (lane j <- column j)
+        uint32_t x = 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) a.task_counts[(size_t)r * a.C * 32 + g] = cnt;
+        for (int j = 0; j < 32; ++j) x |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
+#pragma unroll
+        for (int k = 16; k >= 1; k >>= 1) {
+          const uint32_t ml = k == 16 ? 0x0000FFFFu : k == 8 ? 0x00FF00FFu : k == 4 ? 0x0F0F0F0Fu
+                            : k == 2 ? 0x33333333u : 0x55555555u;
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, x, k);
+          x = (lane & k) ? ((x & ~ml) | ((o & ~ml) >> k)) : ((x & ml) | ((o & ml) << k));
+        }
+        wbuf[(c0 + lane) * kWbStride + widx] = x;
+      }
+      if ((t & 7) == 7 || t + 1 == T) {
+        // the group is complete: 256 request rows of 32 words, top forced,
+        // tail masked; per-group counts for the scans
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+        const uint32_t grp = blockIdx.x * (kLinTiles / 8) + (uint32_t)(t >> 3);
+        const uint64_t wi = (uint64_t)grp * 32 + lane;
+        const uint64_t i0 = a.begin + wi * 32;
+        const int nw = ((t & 7) + 1) * 4;  // words of the group written by the tiles
+        for (int rr = wid; rr < kLinN; rr += kEpiWarps) {
+          const int r = r0 + rr;
+          if (r >= a.R) break;
+          uint32_t w = lane < nw ? wbuf[rr * kWbStride + lane] : 0u;
+          if (wi >= a.W) w = 0;
+          else if (a.end - i0 < 32) w &= (1u << (uint32_t)(a.end - i0)) - 1u;
+          if ((a.flags & AG_FORCE_TOP) && wi < a.W && a.top >= i0 && a.top < i0 + 32) w |= 1u << (uint32_t)(a.top - i0);
+          if (wi < a.W) a.bitmap[(size_t)r * a.W + wi] = w;
+          uint32_t cnt = __popc(w);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+          if (lane == 0 && grp < a.G) a.task_counts[(size_t)r * a.C * 32 + grp] = cnt;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      }
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -265,6 +321,7 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
     a.W = W;
     a.C = C;
     a.flags = flags;
+    a.G = G;
     a.bitmap = bitmap;
     a.task_counts = (uint32_t*)ctx->chunk_counts.p;
     const size_t smem = (size_t)(agb::kLinN + 2 * agb::kLinM) * heads->dim * 2 +
@@ -275,7 +332,8 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
       AG_CUDA(cudaFuncSetAttribute(agb::k_linear_score, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
       attr = true;
     }
-    const dim3 grid(G, (R + agb::kLinN - 1) / agb::kLinN);
+    const uint32_t per_cta = agb::kLinTiles / 8;  // groups per CTA
+    const dim3 grid((G + per_cta - 1) / per_cta, (R + agb::kLinN - 1) / agb::kLinN);
     {
       agb::Launch L(ctx, agb::K_LINEAR_SCORE);
       agb::k_linear_score<<<grid, agb::kLinThreads, smem, s>>>(a);
