@@ -14,4 +14,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_ro
   python bench.py --no-sched --no-deep --no-cpu-baseline --no-config5 --steps 2 --warmup 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_sched_round -s 6 -c 1 -o gpurun_out/${tag}_sched \
   python scripts/sched_ncu.py 8 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_linear_score -s 2 -c 1 -o gpurun_out/${tag}_linear \
+  python scripts/linear_probe.py > /dev/null 2>&1
 ls -la gpurun_out | tail -20
