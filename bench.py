@@ -146,6 +146,19 @@ def ref_sched(rounds):
     return json.loads(out.strip().splitlines()[-1])
 
 
+def absorb_peak():
+    """Measured rng::mix absorb steps/s of this GPU (scripts/ubench/mix_peak),
+    the integer-issue ceiling of the noisy router; None if not built."""
+    exe = os.path.join(ROOT, "scripts", "ubench", "mix_peak")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout
+        return float(json.loads(out.strip().splitlines()[-1])["absorbs_per_s"])
+    except (OSError, ValueError, KeyError, IndexError, subprocess.TimeoutExpired):
+        return None
+
+
 def host_info():
     """CPU model, cores, compiler of the reference build."""
     model = "unknown"
@@ -539,7 +552,21 @@ def run_ours(args):
                  "configs_per_s": REQUESTS_PER_GPU * S / (statistics.median(nms) / 1e3),
                  "ms_per_step": statistics.median(nms), "members_per_step": nmem,
                  "kernel_ms": {k: v[0] / v[1] for k, v in nprof.items()},
-                 "bound": "integer issue (k_route_score)"}
+                 "bound": "integer issue (k_route_noise)"}
+        # k_route_noise against the measured rng::mix absorb rate: with fp = 0
+        # the noise can change exactly the truth bits (one absorb each)
+        mp = absorb_peak()
+        if mp and "k_route_noise" in nprof:
+            kms = nprof["k_route_noise"][0] / nprof["k_route_noise"][1]
+            needed = total_members  # truth bits of the batch (oracle members)
+            if needed:
+                ach = needed / (kms / 1e3)
+                noisy["roofline"] = {"bound": "int-issue", "kernel": "k_route_noise",
+                                     "achieved": ach, "peak": mp, "unit": "absorbs/s",
+                                     "frac": ach / mp,
+                                     "peak_source": "scripts/ubench/mix_peak (measured live)",
+                                     "algorithmic_absorbs_per_launch": needed,
+                                     "avg_launch_ms": kms}
         del nout, nprobe
     sched = run_sched(P, W, dev, args) if rank == 0 and not args.no_sched else None
     deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)

@@ -80,7 +80,7 @@ uint64_t ag_ctx_launch_count(const ag_ctx* ctx);
  * events on the context stream.  ag_ctx_profile_end synchronises the stream
  * and returns, per kernel id (0 .. AG_NUM_KERNELS-1), the summed device
  * milliseconds and launch counts since ag_ctx_profile_begin. */
-#define AG_NUM_KERNELS 10
+#define AG_NUM_KERNELS 11
 int ag_ctx_profile_begin(ag_ctx* ctx);
 int ag_ctx_profile_end(ag_ctx* ctx, double* ms, uint64_t* launches);
 const char* ag_kernel_name(int kernel_id);

@@ -44,7 +44,8 @@ Scratch::~Scratch() {
 
 const char* const kKernelNames[K_NUM_KERNELS] = {
     "k_route_score", "k_chunk_scan", "k_request_scan", "k_route_compact", "k_predict",
-    "k_sched_round", "k_sched_apply", "k_sched_prep", "k_cost_argmin", "k_linear_score"};
+    "k_sched_round", "k_sched_apply", "k_sched_prep", "k_cost_argmin", "k_linear_score",
+    "k_route_noise"};
 
 static_assert(K_NUM_KERNELS == AG_NUM_KERNELS, "kernel id table out of sync with the header");
 

@@ -56,6 +56,7 @@ enum KernelId {
   K_SCHED_PREP,
   K_COST_ARGMIN,
   K_LINEAR_SCORE,
+  K_ROUTE_NOISE,
   K_NUM_KERNELS
 };
 extern const char* const kKernelNames[K_NUM_KERNELS];

@@ -23,9 +23,11 @@
 //   SWAR on packed bytes: ((Q | H) - s.Q) & H == H (all digits < 128).
 //   noisy(c)  = truth ? k >= t_fn : k < t_fp, k = mix({seed, 0xA3, id,
 //             hash_config(c)}) >> 11 (router.cpp:22-28,50-57); the hash chain
-//             is carried incrementally so a scored configuration costs two
-//             splitmix64 finalisers, and only configurations whose verdict
-//             the noise can change are hashed.
+//             is tabulated per space (hash_config is request-independent),
+//             so a scored configuration costs one splitmix64 over a
+//             coalesced table load, lane = bit; only words holding a bit the
+//             noise can change are visited (generic path: the chain carried
+//             incrementally, two finalisers per configuration).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -311,10 +313,7 @@ template <int NT>
 __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   __shared__ PackedSeeds s_seeds[kWarpsPerBlock];
   __shared__ uint32_t s_tr[kWarpsPerBlock][32][33];
-  // phase tables (truth words), then reused as the noise pass's list of
-  // needed bits of half a group (512 x u16 = the table's 1 KB)
-  __shared__ PatTable s_pat[kWarpsPerBlock];
-  static_assert(sizeof(PatTable) >= 512 * sizeof(uint16_t), "needed-bit list overlays the phase table");
+  __shared__ PatTable s_pat[kWarpsPerBlock];  // phase tables (truth words)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t task = blockIdx.x * kWarpsPerBlock + wid;
   if ((uint64_t)task >= (uint64_t)a.R * a.C) return;
@@ -353,8 +352,8 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   const uint32_t i0s = (uint32_t)(a.begin + (uint64_t)wl * 32);  // < 2^32 when wl < wend
   // all 32 words of this lane are full and inside [begin, end)
   const bool full = (uint64_t)i0s + 1024 <= a.end && wl + 32 <= wend;
-  // noisy verdicts deferred to a warp-cooperative pass over the needed bits
-  // when the per-configuration hash is tabulated
+  // noisy verdicts deferred to a word-parallel pass when the
+  // per-configuration hash is tabulated
   const bool defer = a.rt.kind == AG_ROUTER_NOISY && a.hc != nullptr;
   const bool extras = (r1 > r0) || (a.rt.kind == AG_ROUTER_NOISY && !defer) ||
                       ((a.flags & AG_FORCE_TOP) && !defer);
@@ -453,73 +452,6 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
     }
   }
   __syncwarp();
-  if (defer) {
-    // Noisy verdicts (router.cpp:50-57): key = mix({seed, 0xA3, id,
-    // hash_config(c)}) >> 11 = absorb(P, hc[c]) >> 11.  Per half group (16
-    // words = 512 configurations) the needed bits are listed bit-parallel
-    // (word it, lane j -> prefix + popc(need & lanemask_lt)), then every lane
-    // verdicts one listed configuration per pass and flips the bits the noise
-    // changes -- full lanes instead of one bit position per lane.
-    const uint32_t bit = 1u << lane, lt = bit - 1u;
-    uint16_t* lst = reinterpret_cast<uint16_t*>(&s_pat[wid]);
-    for (uint32_t h = 0; h < 64; ++h) {
-      const uint32_t L = h >> 1, it0 = (h & 1u) * 16;
-      const uint32_t wg = wbeg + 32 * L + it0;  // first word of the half group
-      if (wg >= wend) break;
-      const uint64_t ib = a.begin + (uint64_t)wg * 32;
-      // every word of the half group inside [begin, end): no tail masks
-      const bool hfull = wg + 16 <= wend && ib + 512 <= a.end;
-      const uint32_t keep_fn = (a.rt.t_fn > 0) ? 0xffffffffu : 0u, keep_fp = (a.rt.t_fp > 0) ? 0xffffffffu : 0u;
-      uint32_t n = 0;
-      for (uint32_t t = 0; t < 16; ++t) {
-        const uint32_t truth = s_tr[wid][L][it0 + t];
-        uint32_t valid = 0xffffffffu;
-        if (!hfull) {
-          const uint64_t i0 = ib + 32ull * t;
-          valid = (wg + t >= wend || i0 >= a.end) ? 0u
-                : (a.end - i0 >= 32 ? 0xffffffffu : ((1u << (uint32_t)(a.end - i0)) - 1u));
-        }
-        const uint32_t need = ((truth & keep_fn) | (~truth & keep_fp)) & valid;
-        if (need & bit) lst[n + __popc(need & lt)] = (uint16_t)(t * 32 + lane);
-        n += __popc(need);
-      }
-      __syncwarp();
-      // four listed configurations per lane per pass: the table loads of a
-      // pass are in flight together
-      for (uint32_t e0 = 0; e0 < n; e0 += 128) {
-        uint32_t off[4];
-        uint64_t hv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t e = e0 + 32 * u + lane;
-          off[u] = e < n ? lst[e] : 0xffffu;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) hv[u] = off[u] != 0xffffu ? __ldg(a.hc + ib + off[u]) : 0ull;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (off[u] == 0xffffu) continue;
-          const uint32_t t = off[u] >> 5, b = off[u] & 31u;
-          uint32_t* wp = &s_tr[wid][L][it0 + t];
-          const bool truth = (*wp >> b) & 1u;
-          const uint64_t key = absorb(P, hv[u]) >> 11;
-          const bool v = truth ? key >= a.rt.t_fn : key < a.rt.t_fp;
-          if (v != truth) atomicXor(wp, 1u << b);
-        }
-      }
-      __syncwarp();
-    }
-    if ((a.flags & AG_FORCE_TOP) && lane == 0) {
-      const uint64_t tb = a.begin + (uint64_t)wbeg * 32;
-      if (top >= tb && top < tb + 32ull * (wend - wbeg)) {
-        const uint32_t o = (uint32_t)(top - tb);
-        s_tr[wid][(o >> 5) >> 5][(o >> 5) & 31u] |= 1u << (o & 31u);
-      }
-    }
-    __syncwarp();
-    cnt = 0;
-    for (uint32_t it = 0; it < 32; ++it) cnt += __popc(s_tr[wid][lane][it]);
-  }
   uint32_t* brow = a.bitmap + (size_t)r * a.W + wbeg;
   const uint32_t nw = wend - wbeg;
   for (uint32_t it = 0; it < 32; ++it) {
@@ -528,6 +460,74 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   }
   // per-group counts (group = the 32 words of one lane) for the compaction
   a.task_counts[(size_t)task * 32 + lane] = cnt;
+}
+
+// K1n: the noisy router's verdicts over the truth bitmap K1 wrote (router.cpp:
+// 50-57): key = mix({seed, 0xA3, id, hash_config(c)}) >> 11
+// = absorb(P, hc[c]) >> 11 with hash_config tabulated per space.  One block
+// per warp-task, one warp per 4 rows of 32 words; lane j is bit j, so a
+// word's 32 table entries are one coalesced 256-byte load and its new
+// verdicts are ballots.  Only words holding a bit the noise can change are
+// visited, four at a time so their table loads are in flight together.
+// Rewrites the changed words and the per-group counts; forces the top
+// configuration in (AG_FORCE_TOP).  A separate kernel so the hashing work,
+// which varies with each request's truth density, is spread over small
+// units instead of whole-request tasks.
+constexpr int kNoiseRows = 32 / kWarpsPerBlock;
+
+__global__ void __launch_bounds__(kThreads) k_route_noise(ScoreArgs a) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t task = blockIdx.x;
+  const uint32_t r = a.C == 1 ? task : (uint32_t)__umul64hi(task, a.div_c);
+  const uint32_t c = task - r * a.C;
+  const uint64_t P = absorb(absorb(absorb(kMixIV, a.rt.noise_seed), kRouterSalt), __ldg(a.t.request_ids + r));
+  // absorb(P, w) = splitmix(P ^ (w + Pc)) (rng.h:46-49)
+  const uint64_t Pc = kGamma + (P << 6) + (P >> 2);
+  const bool use_fn = a.rt.t_fn > 0, use_fp = a.rt.t_fp > 0;
+  const uint32_t keep_fn = use_fn ? 0xffffffffu : 0u, keep_fp = use_fp ? 0xffffffffu : 0u;
+  const uint64_t top = a.sp.size - 1;
+  const uint32_t wbeg = c * kTaskWords, wend = min(a.W, wbeg + kTaskWords);
+  uint32_t* brow = a.bitmap + (size_t)r * a.W;
+  for (int L = wid * kNoiseRows; L < (wid + 1) * kNoiseRows; ++L) {
+    const uint32_t wg = wbeg + 32u * (uint32_t)L;  // first word of the row
+    if (wg >= wend) break;
+    const uint32_t w = wg + lane;                    // lane t: word wg + t
+    const uint64_t ib = a.begin + (uint64_t)wg * 32;
+    const uint64_t i0 = ib + 32ull * lane;
+    const uint32_t valid = (w >= wend || i0 >= a.end) ? 0u
+                         : (a.end - i0 >= 32 ? 0xffffffffu : ((1u << (uint32_t)(a.end - i0)) - 1u));
+    const uint32_t truth = valid ? brow[w] : 0u;
+    uint32_t word = truth;
+    uint32_t nz = __ballot_sync(0xffffffffu, (((truth & keep_fn) | (~truth & keep_fp)) & valid) != 0u);
+    while (nz) {
+      uint32_t t[4];
+      uint64_t hv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        t[u] = nz ? (uint32_t)(__ffs(nz) - 1) : 32u;
+        nz &= nz - 1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint64_t ci = ib + 32ull * t[u] + lane;
+        hv[u] = (t[u] < 32 && ci < a.end) ? __ldg(a.hc + ci) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (t[u] >= 32) break;  // uniform
+        const uint64_t key = splitmix_step(P ^ (hv[u] + Pc)) >> 11;
+        const uint32_t tr = __shfl_sync(0xffffffffu, truth, (int)t[u]);
+        uint32_t v = tr;
+        if (use_fn) v &= __ballot_sync(0xffffffffu, key >= a.rt.t_fn);
+        if (use_fp) v |= ~tr & __ballot_sync(0xffffffffu, key < a.rt.t_fp);
+        if ((uint32_t)lane == t[u]) word = v & valid;
+      }
+    }
+    if ((a.flags & AG_FORCE_TOP) && valid && top >= i0 && top < i0 + 32) word |= 1u << (uint32_t)(top - i0);
+    if (word != truth) brow[w] = word;
+    const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(word));
+    if (lane == 0) a.task_counts[(size_t)task * 32 + L] = cnt;
+  }
 }
 
 // K2a: one warp per request: exclusive scan of its group counts (32 per
@@ -946,8 +946,14 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   a.task_counts = (uint32_t*)ctx->chunk_counts.p;
   const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
   if (range > 0) {
-    Launch L(ctx, K_ROUTE_SCORE);
-    pick_score(sp->n)(grid, s, a);
+    {
+      Launch L(ctx, K_ROUTE_SCORE);
+      pick_score(sp->n)(grid, s, a);
+    }
+    if (a.hc) {  // noisy router: verdicts over the truth bitmap
+      Launch L(ctx, K_ROUTE_NOISE);
+      k_route_noise<<<(unsigned)ntasks, kThreads, 0, s>>>(a);
+    }
   } else {
     AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
     Launch L(ctx, K_REQUEST_SCAN);

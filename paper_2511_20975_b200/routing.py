@@ -253,7 +253,7 @@ class Device:
 
     def profile_end(self) -> dict:
         """{kernel name: (total device ms, launches)} since profile_begin."""
-        k = 10  # AG_NUM_KERNELS
+        k = 11  # AG_NUM_KERNELS
         ms = (C.c_double * k)()
         n = (C.c_uint64 * k)()
         check(lib().ag_ctx_profile_end(self._h, ms, n))
