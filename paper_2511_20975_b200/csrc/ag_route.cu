@@ -499,28 +499,41 @@ __global__ void __launch_bounds__(kThreads) k_route_noise(ScoreArgs a) {
     const uint32_t truth = valid ? brow[w] : 0u;
     uint32_t word = truth;
     uint32_t nz = __ballot_sync(0xffffffffu, (((truth & keep_fn) | (~truth & keep_fp)) & valid) != 0u);
-    while (nz) {
-      uint32_t t[4];
-      uint64_t hv[4];
+    const uint64_t* hrow = a.hc + ib + lane;  // + 32 t: word t's entries
+    // every word of the row full and inside [begin, end): unguarded loads
+    const bool rfull = wg + 32 <= wend && ib + 1024 <= a.end;
+    auto verdicts = [&](const uint32_t (&t)[4], const uint64_t (&hv)[4], int nb) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        t[u] = nz ? (uint32_t)(__ffs(nz) - 1) : 32u;
-        nz &= nz - 1;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint64_t ci = ib + 32ull * t[u] + lane;
-        hv[u] = (t[u] < 32 && ci < a.end) ? __ldg(a.hc + ci) : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        if (t[u] >= 32) break;  // uniform
+        if (u >= nb) break;  // uniform
         const uint64_t key = splitmix_step(P ^ (hv[u] + Pc)) >> 11;
         const uint32_t tr = __shfl_sync(0xffffffffu, truth, (int)t[u]);
         uint32_t v = tr;
         if (use_fn) v &= __ballot_sync(0xffffffffu, key >= a.rt.t_fn);
         if (use_fp) v |= ~tr & __ballot_sync(0xffffffffu, key < a.rt.t_fp);
         if ((uint32_t)lane == t[u]) word = v & valid;
+      }
+    };
+    while (nz) {
+      uint32_t t[4];
+      uint64_t hv[4];
+      const int nb = min(4, __popc(nz));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        t[u] = nz ? (uint32_t)(__ffs(nz) - 1) : 0u;
+        nz &= nz - 1;
+      }
+      if (rfull && nb == 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) hv[u] = __ldg(hrow + 32 * t[u]);
+        verdicts(t, hv, 4);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint64_t ci = ib + 32ull * t[u] + lane;
+          hv[u] = (u < nb && ci < a.end) ? __ldg(a.hc + ci) : 0ull;
+        }
+        verdicts(t, hv, nb);
       }
     }
     if ((a.flags & AG_FORCE_TOP) && valid && top >= i0 && top < i0 + 32) word |= 1u << (uint32_t)(top - i0);
