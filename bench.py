@@ -140,10 +140,19 @@ def ref_route(sample, threads):
     return json.loads(out.strip().splitlines()[-1])
 
 
-def ref_sched(rounds):
-    out = subprocess.run([REF_BENCH, "sched", str(SCHED_INFLIGHT), str(SCHED_BEAM), str(rounds),
-                          str(SEED), "0"], capture_output=True, text=True, check=True).stdout
+def ref_sched(rounds, beam=SCHED_BEAM, exhaustive=False):
+    out = subprocess.run([REF_BENCH, "sched", str(SCHED_INFLIGHT), str(beam), str(rounds),
+                          str(SEED), "1" if exhaustive else "0"],
+                         capture_output=True, text=True, check=True).stdout
     return json.loads(out.strip().splitlines()[-1])
+
+
+# config-3 variants beside the headline (B = 4, predictor sets): the other
+# beam width SURVEY.md §8(d) names, and exhaustive viable sets (the full
+# accurate set per request, 13.5k configurations on average)
+SCHED_VARIANTS = {"beam1": {"beam": 1, "exhaustive": False, "rounds": 300, "ref_rounds": 310},
+                  "exhaustive": {"beam": SCHED_BEAM, "exhaustive": True, "rounds": 100,
+                                 "ref_rounds": 6}}
 
 
 def absorb_peak():
@@ -228,6 +237,12 @@ def run_reference(args):
     v = statistics.median(vals)
     ms = CPU_SAMPLE_REQUESTS * N_TIERS ** N_AGENTS / v * 1e3
     sched = ref_sched(args.sched_rounds + args.sched_warmup)
+    variants = {}
+    if not args.no_sched_variants:
+        for name, v in SCHED_VARIANTS.items():
+            r = ref_sched(v["ref_rounds"], v["beam"], v["exhaustive"])
+            variants[name] = {"beam": v["beam"], "exhaustive": v["exhaustive"],
+                              "p50_us": r["p50_us"], "p99_us": r["p99_us"], "rounds": r["rounds"]}
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -237,15 +252,16 @@ def run_reference(args):
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "sched": {"p50_us": sched["p50_us"], "p99_us": sched["p99_us"],
                       "mean_us": sched["mean_us"], "rounds": sched["rounds"], "cores": 1,
-                      "decision_hash": sched["hash"],
+                      "decision_hash": sched["hash"], "variants": variants,
                       "what": "beam_schedule per round, reference C++ on one core"}}
     print(json.dumps(line))
 
 
-def run_sched(P, W, dev, args):
+def run_sched(P, W, dev, args, rounds=None, beam=SCHED_BEAM, exhaustive=False):
     """Config 3 on this GPU: p50/p99 of the C-ABI round latency."""
-    c3 = W.Config3(dev, inflight=SCHED_INFLIGHT, rounds=args.sched_rounds + args.sched_warmup,
-                   seed=SEED, beam=SCHED_BEAM)
+    rounds = args.sched_rounds if rounds is None else rounds
+    c3 = W.Config3(dev, inflight=SCHED_INFLIGHT, rounds=rounds + args.sched_warmup,
+                   seed=SEED, beam=beam, exhaustive=exhaustive)
     dev_us, capi_us, free = [], [], []
     weights = list(c3.space.slot_throughput)
 
@@ -569,6 +585,15 @@ def run_ours(args):
                                      "avg_launch_ms": kms}
         del nout, nprobe
     sched = run_sched(P, W, dev, args) if rank == 0 and not args.no_sched else None
+    if sched is not None and not args.no_sched_variants:
+        sched["variants"] = {}
+        for name, v in SCHED_VARIANTS.items():
+            r = run_sched(P, W, dev, args, rounds=v["rounds"], beam=v["beam"],
+                          exhaustive=v["exhaustive"])
+            sched["variants"][name] = {"beam": v["beam"], "exhaustive": v["exhaustive"],
+                                       **{k: r[k] for k in ("p50_us", "p99_us", "device_p50_us",
+                                                            "device_p99_us", "rounds",
+                                                            "by_free_slots")}}
     deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)
     config5 = run_config5() if rank == 0 and not args.no_config5 else None
     clk = clocks.stop()
@@ -631,7 +656,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--sched-rounds", type=int, default=150)
+    ap.add_argument("--sched-rounds", type=int, default=1000)
+    ap.add_argument("--no-sched-variants", action="store_true")
     ap.add_argument("--sched-warmup", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sched", action="store_true")
