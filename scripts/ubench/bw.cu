@@ -1,0 +1,63 @@
+// HBM ceilings by direction (MEASURED_PEAKS.json only has the copy figure):
+// write-only, read-only and copy streams of 16-byte vectors over 512 MiB,
+// grid = 148 SMs x 8 blocks x 256 threads, best of 10, CUDA events.  The
+// compaction kernel (k_route_compact) is write-dominated, so its ceiling is
+// the write-only stream, not the copy.
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a bw.cu -o bw
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+__global__ void k_write(uint4* __restrict__ p, size_t n, uint32_t v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(v, v + 1, v + 2, v + 3);
+}
+__global__ void k_read(const uint4* __restrict__ p, size_t n, uint32_t* sink) {
+  uint32_t x = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const uint4 v = __ldcs(p + i);
+    x ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (x == 0x9e3779b9u) sink[0] = x;
+}
+__global__ void k_copy(const uint4* __restrict__ a, uint4* __restrict__ b, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    b[i] = __ldcs(a + i);
+}
+
+int main() {
+  const size_t bytes = 512ull << 20, n = bytes / 16;
+  uint4 *a, *b;
+  uint32_t* sink;
+  cudaMalloc(&a, bytes);
+  cudaMalloc(&b, bytes);
+  cudaMalloc(&sink, 4);
+  cudaMemset(a, 1, bytes);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int grid = sms * 8;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto best = [&](auto launch) {
+    float bm = 1e30f;
+    for (int r = 0; r < 11; ++r) {
+      cudaEventRecord(e0);
+      launch(r);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (r && ms < bm) bm = ms;
+    }
+    return bm;
+  };
+  const float w = best([&](int r) { k_write<<<grid, 256>>>(b, n, r); });
+  const float ms_memset = best([&](int r) { cudaMemsetAsync(b, r, bytes); });
+  const float rd = best([&](int) { k_read<<<grid, 256>>>(a, n, sink); });
+  const float cp = best([&](int) { k_copy<<<grid, 256>>>(a, b, n); });
+  printf("{\"write_gbs\": %.1f, \"memset_gbs\": %.1f, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, \"bytes\": %zu, \"err\": \"%s\"}\n",
+         bytes / (w * 1e-3) / 1e9, bytes / (ms_memset * 1e-3) / 1e9, bytes / (rd * 1e-3) / 1e9,
+         2.0 * bytes / (cp * 1e-3) / 1e9, bytes, cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
