@@ -82,6 +82,8 @@ int run_route(int n, int m, std::size_t requests, bool noisy, int threads,
   NoisyRouter nr(oracle, 0.0, 0.3, 7);
   const RouterBackend& router = noisy ? static_cast<const RouterBackend&>(nr) : oracle;
   std::vector<std::uint64_t> counts(requests, 0);
+  // per request: sum and sum of squares of the member indices (the digest)
+  std::vector<std::uint64_t> isum(requests, 0), isq(requests, 0);
   std::atomic<std::uint64_t> evals{0};
   const std::uint64_t S = space.size();
 
@@ -89,11 +91,18 @@ int run_route(int n, int m, std::size_t requests, bool noisy, int threads,
   if (!chain_mode) {
     parallel_for(requests, threads, [&](std::size_t id) {
       std::vector<Configuration> members;
+      std::uint64_t sm = 0, sq = 0;
       for (std::uint64_t i = 0; i < S; ++i) {
         Configuration c = space.at_index(i);
-        if (router.evaluate(id, c)) members.push_back(std::move(c));
+        if (router.evaluate(id, c)) {
+          members.push_back(std::move(c));
+          sm += i;
+          sq += i * i;
+        }
       }
       counts[id] = members.size();
+      isum[id] = sm;
+      isq[id] = sq;
     });
   } else {
     ConfigPredictor predictor(space, router);
@@ -109,13 +118,18 @@ int run_route(int n, int m, std::size_t requests, bool noisy, int threads,
   std::uint64_t members = 0;
   for (auto c : counts) members += c;
   if (!chain_mode) {
+    // checksum of per-request checksums, in request order:
+    // D = mix({D, count, sum, sum of squares}) (rng.h mix)
+    std::uint64_t digest = 0x5eed;
+    for (std::size_t r = 0; r < requests; ++r) digest = rng::mix({digest, counts[r], isum[r], isq[r]});
     double configs = static_cast<double>(S) * static_cast<double>(requests);
     std::printf(
         "{\"mode\":\"route\",\"n\":%d,\"m\":%d,\"requests\":%zu,\"router\":\"%s\","
         "\"threads\":%d,\"seconds\":%.6f,\"configs\":%.0f,\"configs_per_s\":%.6e,"
-        "\"members\":%llu}\n",
+        "\"members\":%llu,\"digest\":\"%016llx\"}\n",
         n, m, requests, noisy ? "noisy" : "oracle", threads, dt, configs,
-        configs / dt, static_cast<unsigned long long>(members));
+        configs / dt, static_cast<unsigned long long>(members),
+        static_cast<unsigned long long>(digest));
   } else {
     std::printf(
         "{\"mode\":\"predict\",\"n\":%d,\"m\":%d,\"requests\":%zu,\"router\":\"%s\","
