@@ -239,9 +239,9 @@ def run_reference(args):
     sched = ref_sched(args.sched_rounds + args.sched_warmup)
     variants = {}
     if not args.no_sched_variants:
-        for name, v in SCHED_VARIANTS.items():
-            r = ref_sched(v["ref_rounds"], v["beam"], v["exhaustive"])
-            variants[name] = {"beam": v["beam"], "exhaustive": v["exhaustive"],
+        for name, sv in SCHED_VARIANTS.items():
+            r = ref_sched(sv["ref_rounds"], sv["beam"], sv["exhaustive"])
+            variants[name] = {"beam": sv["beam"], "exhaustive": sv["exhaustive"],
                               "p50_us": r["p50_us"], "p99_us": r["p99_us"], "rounds": r["rounds"]}
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
