@@ -168,6 +168,18 @@ def absorb_peak():
         return None
 
 
+def ubench_bw():
+    """Measured HBM-by-direction and PCIe ceilings (scripts/ubench/bw)."""
+    exe = os.path.join(ROOT, "scripts", "ubench", "bw")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except (OSError, ValueError, IndexError, subprocess.TimeoutExpired):
+        return None
+
+
 def host_info():
     """CPU model, cores, compiler of the reference build."""
     model = "unknown"
@@ -470,6 +482,17 @@ def run_ours(args):
     d2h = hb_counts.nbytes + hb_offsets.nbytes + 4 * total_members
     e2e_ok = int(hb_offsets[-1]) == total_members
     P.lib().ag_host_free(pinned)
+    # the e2e ceiling: the step's PCIe bytes at the measured pinned copy rates
+    bw = ubench_bw() if rank == 0 else None
+    e2e_roof = None
+    if bw and bw.get("pcie_d2h_gbs"):
+        t_min = d2h / (bw["pcie_d2h_gbs"] * 1e9) + h2d / (bw["pcie_h2d_gbs"] * 1e9)
+        e2e_roof = {"bound": "pcie", "bytes_per_step": int(h2d + d2h),
+                    "floor_ms_per_step": t_min * 1e3,
+                    "achieved_ms_per_step": float(e2e_s.item()) / e2e_steps * 1e3,
+                    "frac": t_min / (float(e2e_s.item()) / e2e_steps),
+                    "peak_source": "scripts/ubench/bw (pinned cudaMemcpyAsync, measured live)",
+                    "ubench": bw}
 
     # chain mode (ConfigPredictor::predict, the reference's routing call):
     # the same 10k requests, unbounded budget and the 0.002 s evaluation charge
@@ -623,7 +646,8 @@ def run_ours(args):
         "impl": "ours", "config": workload_config(ws),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "members_ok": bool(e2e_ok and ok_counts),
-                "path": "ag_route_enumerate_host (pinned host indices)"},
+                "path": "ag_route_enumerate_host (pinned host indices)",
+                "roofline": e2e_roof},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
                      "unit": "GB/s", "frac": achieved / hbm, "peak_source": peak_src,
                      "traffic": ncu_traffic(dom),

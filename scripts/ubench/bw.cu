@@ -56,8 +56,16 @@ int main() {
   const float ms_memset = best([&](int r) { cudaMemsetAsync(b, r, bytes); });
   const float rd = best([&](int) { k_read<<<grid, 256>>>(a, n, sink); });
   const float cp = best([&](int) { k_copy<<<grid, 256>>>(a, b, n); });
-  printf("{\"write_gbs\": %.1f, \"memset_gbs\": %.1f, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, \"bytes\": %zu, \"err\": \"%s\"}\n",
+  // PCIe: pinned host <-> device, the e2e path's ceiling
+  void* h = nullptr;
+  cudaHostAlloc(&h, bytes, cudaHostAllocDefault);
+  const float d2h = best([&](int) { cudaMemcpyAsync(h, b, bytes, cudaMemcpyDeviceToHost); });
+  const float h2d = best([&](int) { cudaMemcpyAsync(b, h, bytes, cudaMemcpyHostToDevice); });
+  cudaFreeHost(h);
+  printf("{\"write_gbs\": %.1f, \"memset_gbs\": %.1f, \"read_gbs\": %.1f, \"copy_gbs\": %.1f, "
+         "\"pcie_d2h_gbs\": %.1f, \"pcie_h2d_gbs\": %.1f, \"bytes\": %zu, \"err\": \"%s\"}\n",
          bytes / (w * 1e-3) / 1e9, bytes / (ms_memset * 1e-3) / 1e9, bytes / (rd * 1e-3) / 1e9,
-         2.0 * bytes / (cp * 1e-3) / 1e9, bytes, cudaGetErrorString(cudaGetLastError()));
+         2.0 * bytes / (cp * 1e-3) / 1e9, bytes / (d2h * 1e-3) / 1e9, bytes / (h2d * 1e-3) / 1e9, bytes,
+         cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
