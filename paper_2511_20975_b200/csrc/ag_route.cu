@@ -612,23 +612,33 @@ __global__ void __launch_bounds__(1024)
 }
 
 // K2b: exclusive scan over requests -> offsets[R+1], overflow flag.  One
-// block; each thread owns a contiguous run of requests, read and written in
-// register batches so the loads of a run are in flight together.
+// block; each thread owns a contiguous run of requests.  Runs of up to kKeep
+// counts stay in registers between the two passes (all loads of a run in
+// flight together); longer runs are re-read in batches.
 __global__ void __launch_bounds__(1024)
     k_request_scan(const uint64_t* __restrict__ counts, uint64_t* __restrict__ offsets, int R,
                    uint64_t capacity, uint32_t* __restrict__ overflow) {
-  constexpr int kB = 8;
+  constexpr int kKeep = 16, kB = 8;
   __shared__ uint64_t warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int per = (R + 1023) / 1024;
   const int lo = min(R, (int)threadIdx.x * per), hi = min(R, lo + per);
+  const bool keep = per <= kKeep;
+  uint64_t kv[kKeep];
   uint64_t local = 0;
-  for (int i0 = lo; i0 < hi; i0 += kB) {
-    uint64_t v[kB];
+  if (keep) {
 #pragma unroll
-    for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
+    for (int u = 0; u < kKeep; ++u) kv[u] = lo + u < hi ? __ldg(counts + lo + u) : 0ull;
 #pragma unroll
-    for (int u = 0; u < kB; ++u) local += v[u];
+    for (int u = 0; u < kKeep; ++u) local += kv[u];
+  } else {
+    for (int i0 = lo; i0 < hi; i0 += kB) {
+      uint64_t v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) local += v[u];
+    }
   }
   uint64_t x = local;
 #pragma unroll
@@ -649,16 +659,25 @@ __global__ void __launch_bounds__(1024)
   }
   __syncthreads();
   uint64_t run = warp_sums[wid] + x - local;
-  for (int i0 = lo; i0 < hi; i0 += kB) {
-    uint64_t v[kB];
+  if (keep) {
 #pragma unroll
-    for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
-#pragma unroll
-    for (int u = 0; u < kB; ++u)
-      if (i0 + u < hi) {
-        offsets[i0 + u] = run;
-        run += v[u];
+    for (int u = 0; u < kKeep; ++u)
+      if (lo + u < hi) {
+        offsets[lo + u] = run;
+        run += kv[u];
       }
+  } else {
+    for (int i0 = lo; i0 < hi; i0 += kB) {
+      uint64_t v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
+#pragma unroll
+      for (int u = 0; u < kB; ++u)
+        if (i0 + u < hi) {
+          offsets[i0 + u] = run;
+          run += v[u];
+        }
+    }
   }
   if (hi == R && lo < hi) {
     offsets[R] = run;
