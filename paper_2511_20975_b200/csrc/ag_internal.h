@@ -82,7 +82,7 @@ struct ag_ctx {
   agb::Scratch colmask;  // per-space last-digit masks (route 2-D path)
   agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
   bool hc_ready = false;
-  agb::Scratch cost_args, cost_status;  // runtime-cost argmin
+  agb::Scratch cost_args, cost_status, cost_prefix;  // runtime-cost argmin
   int colmask_m = 0;
   // host-path staging
   agb::Scratch h_truth;

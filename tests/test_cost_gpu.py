@@ -95,3 +95,33 @@ def test_queued_ahead_matches_definition():
                 for mdl in set(((v // 8 ** (n - 1 - a)) % 8).tolist()):
                     want[mdl] += 1
     assert qa == want
+
+
+@pytest.mark.parametrize("n,m", [(8, 12), (25, 2), (26, 2), (32, 2), (4, 200)])
+def test_prefix_table_suffix_lengths(n, m):
+    """The prefix-table split (k digits tabulated, N - k folded per member)
+    for every suffix length the kernel specialises and the generic one:
+    random sorted member lists over the whole space against the oracle."""
+    space = P.ConfigSpace.chain(n, m)
+    dev = P.Device(space)
+    rng = np.random.default_rng(n * 1000 + m)
+    S = m ** n
+    lists = [np.unique(rng.integers(0, S, int(rng.integers(1, 3000)), dtype=np.uint64)).astype(np.uint32)
+             for _ in range(24)]
+    lists.append(np.arange(min(S, 5000), dtype=np.uint32))  # a dense run (many ties)
+    mem, offs = _csr(lists, dev.torch_device)
+    slots = rng.integers(1, 9, m).tolist()
+    occ = [int(rng.integers(0, s + 1)) for s in slots]
+    queued = rng.integers(0, 5, m).tolist()
+    mean = [0.05 + math.exp(-0.3 + 0.01 * i) for i in range(m)]
+    ctx = P.RuntimeCostContext(occ, queued, slots, mean)
+    for kind in (P.PER_INPUT_STATIC, P.PER_INPUT_RUNTIME_COST):
+        ch, est = P.select_per_input(dev, mem, offs, kind, ctx if kind == P.PER_INPUT_RUNTIME_COST else None)
+        ch = ch.cpu().numpy().view(np.uint32)
+        est = est.cpu().numpy()
+        for r, members in enumerate(lists):
+            want, west = O.select_per_input(n, m, space.cost, occ, queued, slots, mean,
+                                            1 if kind == P.PER_INPUT_RUNTIME_COST else 0, members)
+            assert ch[r] == want
+            if kind == P.PER_INPUT_RUNTIME_COST:
+                assert est[r] == west
