@@ -78,7 +78,7 @@ struct ag_ctx {
   std::vector<agb::ProfRecord> prof;
   std::vector<cudaEvent_t> event_pool;
   // routing scratch
-  agb::Scratch chunk_counts, chunk_off, bitmap, counts, offsets, overflow;
+  agb::Scratch chunk_counts, chunk_off, chunk_part, bitmap, counts, offsets, overflow;
   agb::Scratch colmask;  // per-space last-digit masks (route 2-D path)
   agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
   bool hc_ready = false;

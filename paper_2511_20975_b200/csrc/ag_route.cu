@@ -569,45 +569,110 @@ __global__ void __launch_bounds__(kThreads)
   if (lane == 0) counts[r] = carry;
 }
 
-// K2a for long requests (deep spaces): one block per request; each thread
-// sums a contiguous run, a block scan gives the run offsets, then the runs
-// are written.
+// K2a for deep spaces (more than 4096 groups per request): each request's
+// group counts are split into kScanSlices slices, so R * kScanSlices blocks
+// share the work.  Pass 1 sums every slice (coalesced); pass 2 scans each
+// slice from its base (the sum of the earlier slices of its request) in
+// tiles of 8 * 1024 counts staged through shared memory, and the last slice
+// writes the request total.
+constexpr int kScanSlices = 16;
+constexpr int kScanPer = 8;  // counts per thread per tile
+
 __global__ void __launch_bounds__(1024)
-    k_chunk_scan_block(const uint32_t* __restrict__ task_counts, uint64_t* __restrict__ task_off,
-                       uint64_t* __restrict__ counts, uint32_t C) {
+    k_chunk_partial(const uint32_t* __restrict__ task_counts, uint64_t* __restrict__ part, uint32_t C) {
   __shared__ uint64_t warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int r = blockIdx.x;
+  const uint32_t r = blockIdx.y, p = blockIdx.x;
+  const uint32_t slice = (C + kScanSlices - 1) / kScanSlices;
+  const uint32_t lo = min(C, p * slice), hi = min(C, lo + slice);
   const uint32_t* in = task_counts + (size_t)r * C;
-  uint64_t* out = task_off + (size_t)r * C;
-  const uint32_t per = (C + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = min(C, threadIdx.x * per), hi = min(C, lo + per);
-  uint64_t local = 0;
-  for (uint32_t i = lo; i < hi; ++i) local += in[i];
-  uint64_t x = local;
+  uint64_t x = 0;
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += 1024) x += __ldg(in + i);
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_sums[wid] = x;
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) warp_sums[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    const uint64_t v = lane < (int)(blockDim.x / 32) ? warp_sums[lane] : 0;
+    uint64_t v = warp_sums[lane];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) part[(size_t)r * kScanSlices + p] = v;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    k_chunk_scan_slices(const uint32_t* __restrict__ task_counts, const uint64_t* __restrict__ part,
+                        uint64_t* __restrict__ task_off, uint64_t* __restrict__ counts, uint32_t C) {
+  __shared__ uint32_t s_in[kScanPer * 1024];
+  __shared__ uint64_t warp_sums[32];
+  __shared__ uint64_t s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t r = blockIdx.y, p = blockIdx.x;
+  const uint32_t slice = (C + kScanSlices - 1) / kScanSlices;
+  const uint32_t lo = min(C, p * slice), hi = min(C, lo + slice);
+  const uint32_t* in = task_counts + (size_t)r * C;
+  uint64_t* out = task_off + (size_t)r * C;
+  if (wid == 0) {
+    const uint64_t v = lane < (int)p ? part[(size_t)r * kScanSlices + lane] : 0ull;
     uint64_t z = v;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
-      if (lane >= o) z += y;
+    for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+    if (lane == 0) s_base = z;
+    if (p == kScanSlices - 1 && lane == 0) {
+      uint64_t tot = 0;
+      for (int q = 0; q < kScanSlices; ++q) tot += part[(size_t)r * kScanSlices + q];
+      counts[r] = tot;
     }
-    if (lane < (int)(blockDim.x / 32)) warp_sums[lane] = z - v;
-    if (lane == 31) counts[r] = z;
   }
   __syncthreads();
-  uint64_t run = warp_sums[wid] + x - local;
-  for (uint32_t i = lo; i < hi; ++i) {
-    out[i] = run;
-    run += in[i];
+  uint64_t carry = s_base;
+  for (uint32_t t0 = lo; t0 < hi; t0 += kScanPer * 1024) {
+    const uint32_t n = min(hi - t0, (uint32_t)(kScanPer * 1024));
+#pragma unroll
+    for (int u = 0; u < kScanPer; ++u) {
+      const uint32_t i = u * 1024 + threadIdx.x;
+      s_in[i] = i < n ? __ldg(in + t0 + i) : 0u;
+    }
+    __syncthreads();
+    uint32_t v[kScanPer];
+    uint64_t local = 0;
+#pragma unroll
+    for (int u = 0; u < kScanPer; ++u) {
+      v[u] = s_in[threadIdx.x * kScanPer + u];
+      local += v[u];
+    }
+    uint64_t x = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t w = warp_sums[lane];
+      uint64_t z = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      warp_sums[lane] = z - w;  // exclusive warp prefix
+    }
+    __syncthreads();
+    uint64_t run = carry + warp_sums[wid] + x - local;
+    const uint32_t b = threadIdx.x * kScanPer;
+#pragma unroll
+    for (int u = 0; u < kScanPer; ++u) {
+      if (b + u < n) out[t0 + b + u] = run;
+      run += v[u];
+    }
+    // the tile total, for the next tile's carry
+    __syncthreads();  // every thread has read its warp prefix
+    if (threadIdx.x == 1023) warp_sums[0] = run;  // run after the last element
+    __syncthreads();
+    carry = warp_sums[0];
+    __syncthreads();
   }
 }
 
@@ -1003,14 +1068,23 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
 int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, uint32_t* bitmap,
                      uint64_t* offsets, const ag_route_out* out) {
   cudaStream_t s = ctx->stream;
-  {
+  if (C * 32 <= 4096) {
     Launch L(ctx, K_CHUNK_SCAN);
-    if (C * 32 <= 4096)
-      k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
-          (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
-    else
-      k_chunk_scan_block<<<R, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
-                                            (uint64_t*)ctx->chunk_off.p, out->counts, C * 32);
+    k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
+        (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
+  } else {
+    int rc = ctx->chunk_part.ensure((size_t)R * kScanSlices * 8);
+    if (rc) return rc;
+    const dim3 g(kScanSlices, R);
+    {
+      Launch L(ctx, K_CHUNK_SCAN);
+      k_chunk_partial<<<g, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
+                                         (uint64_t*)ctx->chunk_part.p, C * 32);
+    }
+    Launch L(ctx, K_CHUNK_SCAN);
+    k_chunk_scan_slices<<<g, 1024, 0, s>>>((const uint32_t*)ctx->chunk_counts.p,
+                                           (const uint64_t*)ctx->chunk_part.p,
+                                           (uint64_t*)ctx->chunk_off.p, out->counts, C * 32);
   }
   {
     Launch L(ctx, K_REQUEST_SCAN);

@@ -131,6 +131,16 @@ def test_deep_space_range_8x12():
         _check_against_oracle(dev, space, batch, router, lo, lo + 3_000_000 + 17)
 
 
+def test_deep_space_long_window_multi_slice_scan():
+    """More than 4096 32-word groups per request: the sliced group scan
+    (k_chunk_partial / k_chunk_scan_slices) instead of the warp scan."""
+    space = P.ConfigSpace.chain(8, 12)
+    batch = P.AccuracyBatch.generate(space, P.GenParams(), 3, seed=5)
+    dev = P.Device(space)
+    lo = space.size // 5 + 3
+    _check_against_oracle(dev, space, batch, P.OracleRouter(), lo, lo + 9_000_000 + 13)
+
+
 def test_host_path_and_capacity():
     space = P.ConfigSpace.chain(4, 6)
     batch = P.AccuracyBatch.generate(space, P.GenParams(), 100, seed=2)
