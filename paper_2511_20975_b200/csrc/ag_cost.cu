@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const CostArgs* 
   const uint32_t m = (uint32_t)m_, mk = A.mk;
   const uint64_t div_m = A.sp.div_m, div_mk = A.div_mk;
   const double2* __restrict__ prefix = A.prefix;
+  const bool runtime = A.kind != 0;
   double be = INFINITY, bc = INFINITY;
   uint32_t bi = 0xffffffffu;
   bool missing = false;
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const CostArgs* 
         c += s_cost[dg];
       }
       missing |= isnan(e);  // a NaN term (missing tier) anywhere in the fold
-      if (A.kind == 0) e = 0.0;
+      if (!runtime) e = 0.0;
       if (key_less(e, c, idx[u], be, bc, bi)) be = e, bc = c, bi = idx[u];
     }
   }
