@@ -788,29 +788,29 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       __syncwarp();
       { const long long t = clock64(); tw[1] += t - tp; tp = t; }
       // rank under state_better, then the lower child index (never reached:
-      // distinct children hold distinct lists); batches of 4 with every
-      // shared-memory load issued up front, comparisons branch-free
+      // distinct children hold distinct lists).  Pass 1 counts the children
+      // with a strictly higher utilization (one 64-bit compare each, keys
+      // read four at a time); pass 2 compares the remaining keys only
+      // against the children with the same utilization (match_any group).
+      const unsigned vmask = __ballot_sync(kFull, valid);
+      const unsigned tie = __match_any_sync(kFull, ku) & vmask & ~(1u << lane);
       unsigned rank = 0xffffffffu;
       if (valid) {
         rank = 0;
         for (int c0 = 0; c0 < nchild; c0 += 4) {
-          RankKey y[4];
-          uint64_t rr[4];
+          uint64_t yu[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) y[u] = s_rk[min(c0 + u, 31)];
+          for (int u = 0; u < 4; ++u) yu[u] = s_rk[min(c0 + u, 31)].ku;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) rr[u] = R[y[u].pk & 31u][par];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int c2 = c0 + u;
-            const uint32_t ym1 = y[u].pk >> 8;
-            const uint64_t yk = ym1 ? key_base | (uint64_t)(ym1 - 1) : kEnd;
-            const bool lexb = lex_before((int)(y[u].pk & 31u) == par, rr[u], yk, ck);
-            const bool yb = (y[u].ku > ku) |
-                            ((y[u].ku == ku) & ((y[u].kf > kf) | ((y[u].kf == kf) & ((y[u].sk < sk) |
-                                                                                     ((y[u].sk == sk) & lexb)))));
-            rank += (c2 < nchild) & (c2 != lane) & yb;
-          }
+          for (int u = 0; u < 4; ++u) rank += (c0 + u < nchild) & (yu[u] > ku);
+        }
+        for (unsigned tb = tie; tb; tb &= tb - 1) {
+          const RankKey y = s_rk[__ffs(tb) - 1];
+          const uint64_t rr = R[y.pk & 31u][par];
+          const uint32_t ym1 = y.pk >> 8;
+          const uint64_t yk = ym1 ? key_base | (uint64_t)(ym1 - 1) : kEnd;
+          const bool lexb = lex_before((int)(y.pk & 31u) == par, rr, yk, ck);
+          rank += (y.kf > kf) | ((y.kf == kf) & ((y.sk < sk) | ((y.sk == sk) & lexb)));
         }
       }
       // nested retention (scheduler.cpp:351-370): level w adopts the best
