@@ -110,7 +110,7 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r,
                     uint64_t begin, uint64_t end, uint32_t flags,
                     const ag_route_out* out);
 int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, uint32_t* bitmap,
-                     uint64_t* offsets, const ag_route_out* out);
+                     uint64_t* offsets, const ag_route_out* out, bool scanned = false);
 int route_compact(ag_ctx* ctx, int R, uint64_t begin, uint64_t end, const uint32_t* bitmap,
                   const uint64_t* offsets, uint32_t* indices, uint64_t capacity);
 int make_router(const ag_router* r, RouterDev* out);

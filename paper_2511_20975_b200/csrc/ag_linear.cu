@@ -260,10 +260,6 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
 
 }  // namespace
 
-// scans + compaction of a verdict bitmap produced by a scoring kernel
-// (ag_route.cu)
-int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, uint32_t* bitmap,
-                     uint64_t* offsets, const ag_route_out* out);
 
 }  // namespace agb
 

@@ -292,6 +292,11 @@ struct ScoreArgs {
   const uint64_t* hc;  // hash_config(c) per canonical index (noisy router), or null
   uint32_t* bitmap;  // [R * W]
   uint32_t* task_counts;
+  // C == 1 (a task is a whole request): the group scan (K2a) fused into the
+  // scoring kernel -- group offsets and the request's count written here
+  int fuse_scan;
+  uint64_t* task_off;
+  uint64_t* counts;
 };
 
 // Phase-pattern path (M*M >= 32 and few phases): a 32-index word starting at
@@ -460,6 +465,16 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   }
   // per-group counts (group = the 32 words of one lane) for the compaction
   a.task_counts[(size_t)task * 32 + lane] = cnt;
+  if (a.fuse_scan && !defer) {  // K2a here: exclusive scan over the 32 groups
+    uint64_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    a.task_off[(size_t)task * 32 + lane] = x - cnt;
+    if (lane == 31) a.counts[r] = x;
+  }
 }
 
 // K1n: the noisy router's verdicts over the truth bitmap K1 wrote (router.cpp:
@@ -540,6 +555,20 @@ __global__ void __launch_bounds__(kThreads) k_route_noise(ScoreArgs a) {
     if (word != truth) brow[w] = word;
     const uint32_t cnt = __reduce_add_sync(0xffffffffu, (uint32_t)__popc(word));
     if (lane == 0) a.task_counts[(size_t)task * 32 + L] = cnt;
+  }
+  if (a.fuse_scan) {  // K2a here: exclusive scan over the task's 32 groups
+    __syncthreads();
+    if (wid == 0) {
+      const uint32_t v = a.task_counts[(size_t)task * 32 + lane];
+      uint64_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      a.task_off[(size_t)task * 32 + lane] = x - v;
+      if (lane == 31) a.counts[r] = x;
+    }
   }
 }
 
@@ -1041,6 +1070,9 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   a.hc = rt.kind == AG_ROUTER_NOISY ? ensure_hash_table(ctx) : nullptr;
   a.bitmap = bitmap;
   a.task_counts = (uint32_t*)ctx->chunk_counts.p;
+  a.fuse_scan = C == 1 ? 1 : 0;
+  a.task_off = (uint64_t*)ctx->chunk_off.p;
+  a.counts = out->counts;
   const dim3 grid((unsigned)((ntasks + kWarpsPerBlock - 1) / kWarpsPerBlock));
   if (range > 0) {
     {
@@ -1059,16 +1091,18 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
     AG_CUDA(cudaGetLastError());
     return AG_OK;
   }
-  return finish_enumerate(ctx, R, W, C, begin, bitmap, offsets, out);
+  return finish_enumerate(ctx, R, W, C, begin, bitmap, offsets, out, a.fuse_scan != 0);
 }
 
 // K2 scans + K3 compaction of a verdict bitmap [R][W] whose per-group counts
 // ([R][C*32], 32-word groups) are in ctx->chunk_counts: shared by the oracle /
 // noisy scoring kernel and the learned router (ag_linear.cu).
 int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, uint32_t* bitmap,
-                     uint64_t* offsets, const ag_route_out* out) {
+                     uint64_t* offsets, const ag_route_out* out, bool scanned) {
   cudaStream_t s = ctx->stream;
-  if (C * 32 <= 4096) {
+  if (scanned) {
+    // group offsets and counts already written by the scoring kernel
+  } else if (C * 32 <= 4096) {
     Launch L(ctx, K_CHUNK_SCAN);
     k_chunk_scan<<<(R + kWarpsPerBlock - 1) / kWarpsPerBlock, kThreads, 0, s>>>(
         (const uint32_t*)ctx->chunk_counts.p, (uint64_t*)ctx->chunk_off.p, out->counts, C * 32, R);
