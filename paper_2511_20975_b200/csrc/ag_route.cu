@@ -706,76 +706,72 @@ __global__ void __launch_bounds__(1024)
 }
 
 // K2b: exclusive scan over requests -> offsets[R+1], overflow flag.  One
-// block; each thread owns a contiguous run of requests.  Runs of up to kKeep
-// counts stay in registers between the two passes (all loads of a run in
-// flight together); longer runs are re-read in batches.
+// block, tiles of 4 x 1024 counts: loaded and stored coalesced through shared
+// memory (a single SM's L1 is the limit: per-thread contiguous runs would
+// cost one sector request per element), each thread scanning 4 contiguous
+// counts of the tile; the tile total carries to the next tile.
+constexpr int kReqPer = 4;
+
 __global__ void __launch_bounds__(1024)
     k_request_scan(const uint64_t* __restrict__ counts, uint64_t* __restrict__ offsets, int R,
                    uint64_t capacity, uint32_t* __restrict__ overflow) {
-  constexpr int kKeep = 16, kB = 8;
+  __shared__ uint64_t s_t[kReqPer * 1024];
   __shared__ uint64_t warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int per = (R + 1023) / 1024;
-  const int lo = min(R, (int)threadIdx.x * per), hi = min(R, lo + per);
-  const bool keep = per <= kKeep;
-  uint64_t kv[kKeep];
-  uint64_t local = 0;
-  if (keep) {
+  uint64_t carry = 0;
+  for (int t0 = 0; t0 < R; t0 += kReqPer * 1024) {
+    const int n = min(R - t0, kReqPer * 1024);
 #pragma unroll
-    for (int u = 0; u < kKeep; ++u) kv[u] = lo + u < hi ? __ldg(counts + lo + u) : 0ull;
-#pragma unroll
-    for (int u = 0; u < kKeep; ++u) local += kv[u];
-  } else {
-    for (int i0 = lo; i0 < hi; i0 += kB) {
-      uint64_t v[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
-#pragma unroll
-      for (int u = 0; u < kB; ++u) local += v[u];
+    for (int u = 0; u < kReqPer; ++u) {
+      const int i = u * 1024 + threadIdx.x;
+      s_t[i] = i < n ? __ldg(counts + t0 + i) : 0ull;
     }
-  }
-  uint64_t x = local;
+    __syncthreads();
+    uint64_t v[kReqPer], local = 0;
 #pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) warp_sums[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    uint64_t v = warp_sums[lane], z = v;
+    for (int u = 0; u < kReqPer; ++u) {
+      v[u] = s_t[threadIdx.x * kReqPer + u];
+      local += v[u];
+    }
+    uint64_t x = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
-      if (lane >= o) z += y;
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
     }
-    warp_sums[lane] = z - v;  // exclusive warp prefix
-  }
-  __syncthreads();
-  uint64_t run = warp_sums[wid] + x - local;
-  if (keep) {
+    if (lane == 31) warp_sums[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t w = warp_sums[lane];
+      uint64_t z = w;
 #pragma unroll
-    for (int u = 0; u < kKeep; ++u)
-      if (lo + u < hi) {
-        offsets[lo + u] = run;
-        run += kv[u];
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
       }
-  } else {
-    for (int i0 = lo; i0 < hi; i0 += kB) {
-      uint64_t v[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) v[u] = i0 + u < hi ? __ldg(counts + i0 + u) : 0ull;
-#pragma unroll
-      for (int u = 0; u < kB; ++u)
-        if (i0 + u < hi) {
-          offsets[i0 + u] = run;
-          run += v[u];
-        }
+      warp_sums[lane] = z - w;  // exclusive warp prefix
     }
+    __syncthreads();
+    uint64_t run = carry + warp_sums[wid] + x - local;
+#pragma unroll
+    for (int u = 0; u < kReqPer; ++u) {
+      s_t[threadIdx.x * kReqPer + u] = run;
+      run += v[u];
+    }
+    __syncthreads();  // tile offsets staged; every warp prefix read
+#pragma unroll
+    for (int u = 0; u < kReqPer; ++u) {
+      const int i = u * 1024 + threadIdx.x;
+      if (i < n) offsets[t0 + i] = s_t[i];
+    }
+    if (threadIdx.x == 1023) warp_sums[0] = run;  // the running total after this tile
+    __syncthreads();
+    carry = warp_sums[0];
+    __syncthreads();
   }
-  if (hi == R && lo < hi) {
-    offsets[R] = run;
-    if (overflow) *overflow = run > capacity ? 1u : 0u;
+  if (threadIdx.x == 0) {
+    offsets[R] = carry;
+    if (overflow) *overflow = carry > capacity ? 1u : 0u;
   }
 }
 
