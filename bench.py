@@ -496,7 +496,7 @@ def run_ours(args):
     e2e_ok = int(hb_offsets[-1]) == total_members
     P.lib().ag_host_free(pinned)
     # the e2e ceiling: the step's PCIe bytes at the measured pinned copy rates
-    bw = ubench_bw() if rank == 0 else None
+    bw = ubench_bw() if rank == 0 and not args.no_ubench else None
     e2e_roof = None
     if bw and bw.get("pcie_d2h_gbs"):
         t_min = d2h / (bw["pcie_d2h_gbs"] * 1e9) + h2d / (bw["pcie_h2d_gbs"] * 1e9)
@@ -607,7 +607,7 @@ def run_ours(args):
                  "bound": "integer issue (k_route_noise)"}
         # k_route_noise against the measured rng::mix absorb rate: with fp = 0
         # the noise can change exactly the truth bits (one absorb each)
-        mp = absorb_peak()
+        mp = absorb_peak() if not args.no_ubench else None
         if mp and "k_route_noise" in nprof:
             kms = nprof["k_route_noise"][0] / nprof["k_route_noise"][1]
             needed = total_members  # truth bits of the batch (oracle members)
@@ -703,6 +703,8 @@ def main():
     ap.add_argument("--no-noisy", action="store_true")
     ap.add_argument("--no-chain", action="store_true")
     ap.add_argument("--no-linear", action="store_true")
+    ap.add_argument("--no-ubench", action="store_true",
+                    help="skip the PCIe / absorb-rate microbenchmarks (e.g. under ncu)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
