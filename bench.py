@@ -607,7 +607,7 @@ def run_ours(args):
                  "bound": "integer issue (k_route_noise)"}
         # k_route_noise against the measured rng::mix absorb rate: with fp = 0
         # the noise can change exactly the truth bits (one absorb each)
-        mp = absorb_peak() if not args.no_ubench else None
+        mp = absorb_peak() if rank == 0 and not args.no_ubench else None
         if mp and "k_route_noise" in nprof:
             kms = nprof["k_route_noise"][0] / nprof["k_route_noise"][1]
             needed = total_members  # truth bits of the batch (oracle members)
