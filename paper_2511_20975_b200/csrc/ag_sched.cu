@@ -58,6 +58,25 @@
 
 #include "ag_internal.h"
 
+// Per-step phase timers of the walker (find / build / rank / adopt cycles,
+// ag_sched_round_timing slots 5-8): diagnostics, compiled in on request only
+// (-DAG_SCHED_PHASE_TIMERS=1) -- four clock reads per beam step otherwise.
+#ifndef AG_SCHED_PHASE_TIMERS
+#define AG_SCHED_PHASE_TIMERS 0
+#endif
+#if AG_SCHED_PHASE_TIMERS
+#define AG_PHASE_TICK(k)            \
+  do {                              \
+    const long long t_ = clock64(); \
+    tw[k] += t_ - tp;               \
+    tp = t_;                        \
+  } while (0)
+#else
+#define AG_PHASE_TICK(k) \
+  do {                   \
+  } while (0)
+#endif
+
 namespace agb {
 
 namespace {
@@ -644,7 +663,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       }
       j0 = min(j0 + 32, (int)h);
     }
-    { const long long t = clock64(); tw[0] += t - tp; tp = t; }
+    AG_PHASE_TICK(0);
     if (found < 0) break;
     j = found;
     const Cand cr = recf(j);
@@ -786,7 +805,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         s_rk[lane] = rk;
       }
       __syncwarp();
-      { const long long t = clock64(); tw[1] += t - tp; tp = t; }
+      AG_PHASE_TICK(1);
       // rank under state_better, then the lower child index (never reached:
       // distinct children hold distinct lists).  Pass 1 counts the children
       // with a strictly higher utilization (one 64-bit compare each, keys
@@ -879,7 +898,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         }
       }
       __syncwarp();
-      { const long long t = clock64(); tw[1] += t - tp; tp = t; }
+      AG_PHASE_TICK(1);
       auto keyf = [&](int c) -> uint64_t {
         return children[c].eng >= 0 ? key_base | (uint64_t)(uint32_t)e_model[children[c].eng] : kEnd;
       };
@@ -926,7 +945,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         c_eng = chd.eng;
       }
     }
-    { const long long t = clock64(); tw[2] += t - tp; tp = t; }
+    AG_PHASE_TICK(2);
     // adopt: picked child w becomes state w of the next beam
     const int nxt = cur ^ 1;
     const bool mine = lane < npick;
@@ -994,7 +1013,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     __syncwarp();
     cur = nxt;
     nst = npick;
-    { const long long t = clock64(); tw[3] += t - tp; tp = t; }
+    AG_PHASE_TICK(3);
   }
   // producers stop at their next chunk boundary
   if (lane == 0) *(volatile unsigned*)&s_walk_done = 1u;
