@@ -164,6 +164,8 @@ class SchedSession:
         self.walk_counts = t[9:11].astype(np.int64)
         self.ctx_cycles = self.walk_counts
         self.chunk_us = np.diff(np.concatenate([[float(t[1])], t[11:15].astype(np.float64)])) / 1e3
+        # producers' end relative to the walk's end (us; > 0: they finished later)
+        self.producers_after_walk_us = (float(t[15]) - float(t[3])) / 1e3 if t[15] else 0.0
         return np.diff(t[:5].astype(np.float64)) / 1e3
 
     def last_round_us(self) -> float:
