@@ -148,7 +148,7 @@ struct RoundArgs {
   uint32_t* gmask;  // candidates beyond shared memory
   Cand* grec;
   int cand_cap, hist_cap;
-  int ebm_nw;   // words per engine bitmap over candidates (0: no bitmaps)
+  int wor_cap;  // 32-candidate windows: the union of their engine masks
   Node* gnodes;
   int max_nodes;
   int max_children;
@@ -309,10 +309,10 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   Cand* c_rec = reinterpret_cast<Cand*>(h_rat + (size_t)A.hist_cap * A.M);
   uint32_t* c_mask = reinterpret_cast<uint32_t*>(c_rec + A.cand_cap);
   uint32_t* h_cnt = c_mask + A.cand_cap;
-  // per engine, a bitmap over candidates (bit k: candidate k's mask holds the
-  // engine): the walker finds the next candidate meeting the free engines
-  // 1024 candidates per ballot without reading them
-  uint32_t* s_ebm = h_cnt + (size_t)A.hist_cap * A.M;
+  // per window of 32 candidates, the union of their masks: the walker skips
+  // a published window whose union misses every free engine without reading
+  // its candidates
+  uint32_t* s_wor = h_cnt + (size_t)A.hist_cap * A.M;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int N = A.N, M = A.M, B = A.B;
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       *A.async_status = 0;
     }
   }
-  for (int i = tid; i < A.ebm_nw * A.eng.E; i += kRoundThreads) s_ebm[i] = 0u;
+  for (int i = tid; i < A.wor_cap; i += kRoundThreads) s_wor[i] = 0u;
   if (tid < kMaxEng) {
     e_model[tid] = A.eng.model[tid];
     e_slots[tid] = A.eng.slots[tid];
@@ -524,9 +524,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
               A.gmask[cw - A.cand_cap] = em & U0;
               A.grec[cw - A.cand_cap] = r;
             }
-            if ((cw >> 5) < A.ebm_nw)  // before the chunk's release
-              for (uint32_t eb = em & U0; eb; eb &= eb - 1)
-                atomicOr(&s_ebm[(__ffs(eb) - 1) * A.ebm_nw + (cw >> 5)], 1u << (cw & 31));
+            atomicOr(&s_wor[cw >> 5], em & U0);  // before the chunk's release
             ++cw;
           }
           ++pos;
@@ -672,33 +670,20 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         break;
       }
       j0 = min(j0 + 32, (int)h);
-      if (A.ebm_nw == 0) continue;
-      // engine bitmaps: the first published candidate >= j0 whose mask meets
-      // U, one 32-candidate word per lane (1024 candidates per ballot)
+      // skip published windows whose mask union misses U, 32 windows per
+      // ballot; stop at the first window that may match or is not complete
       for (;;) {
-        const int w0 = j0 >> 5, wl = w0 + lane, lo = wl * 32;
-        uint32_t word = 0;
-        if (wl < A.ebm_nw && lo < (int)have) {
-          for (uint32_t uu = U; uu; uu &= uu - 1) word |= s_ebm[(__ffs(uu) - 1) * A.ebm_nw + wl];
-          if (lo < j0) word &= ~0u << (j0 - lo);                                // before j0
-          if (lo + 32 > (int)have) word &= (1u << ((int)have - lo)) - 1u;       // unpublished
-        }
-        const unsigned b2 = __ballot_sync(kFull, word != 0u);
-        if (b2) {
-          const int src = __ffs(b2) - 1;
-          const uint32_t wd = __shfl_sync(kFull, word, src);
-          found = (w0 + src) * 32 + __ffs(wd) - 1;
-          base = maskf(found);
-          break;
-        }
-        if ((w0 + 32) * 32 < (int)have) {
+        const int w0 = j0 >> 5, wl = w0 + lane;
+        const bool pub = (unsigned)(wl + 1) * 32u <= have;
+        const unsigned sb = __ballot_sync(kFull, !pub || (s_wor[pub ? wl : 0] & U) != 0u);
+        if (sb == 0u) {
           j0 = (w0 + 32) * 32;
           continue;
         }
-        j0 = (int)have;  // every published candidate scanned: wait for more
+        const int first = __ffs(sb) - 1;
+        if (first > 0) j0 = (w0 + first) * 32;
         break;
       }
-      if (found >= 0) break;
     }
     AG_PHASE_TICK(0);
     if (found < 0) break;
@@ -1628,13 +1613,9 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   const size_t max_dyn = 227 * 1024 - static_bytes;
   const size_t fixed = sizeof(Node) * kSmemNodes + sizeof(Child) * (size_t)max_children;
   if (fixed > max_dyn) return fail(AG_ERR_VALIDATION, "beam too wide for one CTA");
-  // engine bitmaps over the round's candidates (<= its ready pairs), when
-  // they fit in 32 KB
-  int ebm_nw = (int)((s->npairs + 31) / 32) + 1;
-  if ((size_t)ebm_nw * 4 * (size_t)std::max(1, ed.E) > 32 * 1024) ebm_nw = 0;
-  const size_t ebm_bytes = (size_t)ebm_nw * 4 * (size_t)std::max(1, ed.E);
-  if (fixed + ebm_bytes > max_dyn) return fail(AG_ERR_VALIDATION, "beam too wide for one CTA");
-  size_t room = max_dyn - fixed - ebm_bytes;
+  const int wor_cap = (int)((max_pairs + 31) / 32) + 1;
+  if (fixed + 4 * (size_t)wor_cap > max_dyn) return fail(AG_ERR_VALIDATION, "beam too wide for one CTA");
+  size_t room = max_dyn - fixed - 4 * (size_t)wor_cap;
   // the walk visits the head of the candidate list (engines fill quickly):
   // histogram rows and ratios are staged for that head only
   const size_t row_bytes = (size_t)s->M * (sizeof(double) + sizeof(uint32_t));
@@ -1644,7 +1625,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   const int cand_cap = (int)std::min<size_t>(max_pairs, room / (sizeof(Cand) + 4) & ~(size_t)3);
   hist_cap = std::min(hist_cap, cand_cap & ~1);
   const size_t dyn = fixed + (size_t)hist_cap * row_bytes + (size_t)cand_cap * (sizeof(Cand) + 4) +
-                     ebm_bytes;
+                     4 * (size_t)wor_cap;
   const size_t g_over = max_pairs > (size_t)cand_cap ? max_pairs - cand_cap : 1;
   if ((rc = s->d_cpos.ensure(g_over * 4)) || (rc = s->d_det.ensure(g_over * sizeof(Cand))) ||
       (rc = s->d_nodes.ensure((size_t)std::max(1, max_nodes - kSmemNodes) * sizeof(Node))))
@@ -1686,7 +1667,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.gmask = (uint32_t*)s->d_cpos.p;
   A.grec = (Cand*)s->d_det.p;
   A.cand_cap = cand_cap;
-  A.ebm_nw = ebm_nw;
+  A.wor_cap = wor_cap;
   A.hist_cap = hist_cap;
   A.gnodes = (Node*)s->d_nodes.p;
   A.max_nodes = max_nodes;
