@@ -8,18 +8,21 @@
 // E: request embeddings [R][D] bf16; H: one linear head per canonical
 // configuration [S][D] bf16; bias [S] fp32.  Scoring every configuration of a
 // batch is the dense contraction E . H^T (2 R S D flops), run as tcgen05 tiles:
-//   * one CTA owns a tile of 256 requests (the B operand, loaded once) and a
-//     chunk of 8 configuration tiles of 128 (A operands, double buffered),
-//     i.e. 1024 configurations = one 32-word bitmap group per request;
+//   * one CTA owns a tile of 256 requests (two 128-row A operands, loaded
+//     once) and a chunk of 16 configuration tiles of 128 (the B operand,
+//     double buffered), i.e. 2048 configurations = two 32-word bitmap groups
+//     per request;
 //   * operands sit in shared memory in the canonical no-swizzle K-major
 //     layout (8-row x 16-byte core matrices, K-chunks 128 B apart); one thread
-//     issues tcgen05.mma kind::f16 (M 128, N 256, K 16) into a TMEM
-//     accumulator (two 256-column buffers) and commits to an mbarrier;
-//   * the epilogue warps (4 per TMEM lane quarter) read 32 accumulator
-//     columns at a time with tcgen05.ld, threshold against the row's bias
-//     into a 32-bit row mask, and a 32x32 bit transpose across the warp turns
-//     32 configurations into each request's bitmap word -- the verdict bitmap comes out in the same [R][W] layout
-//     as k_route_score, so the scans and k_route_compact finish the job.
+//     issues tcgen05.mma kind::f16 (M 128, N 128, K 16), one per request half,
+//     into TMEM accumulators (two stages x two halves x 128 columns) and
+//     commits to an mbarrier;
+//   * TMEM lane = request, column = configuration: an epilogue thread reads 32
+//     consecutive configurations of its request with one tcgen05.ld and
+//     thresholds them straight into that request's bitmap word (thresholds
+//     broadcast from shared memory; no transpose) -- the verdict bitmap comes
+//     out in the same [R][W] layout as k_route_score, so the scans and
+//     k_route_compact finish the job.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,10 +33,11 @@
 namespace agb {
 namespace {
 
-constexpr int kLinM = 128;        // configurations per MMA tile
-constexpr int kLinN = 256;        // requests per CTA
+constexpr int kLinM = 128;        // requests per MMA (one TMEM lane each)
+constexpr int kLinR = 256;        // requests per CTA (two MMAs per K step)
+constexpr int kLinN = 128;        // configurations per tile (MMA N)
 constexpr int kLinTiles = 16;     // configuration tiles per CTA (2 groups of 1024)
-constexpr int kEpiWarps = 16;     // epilogue: 4 per TMEM lane quarter, 64 columns each
+constexpr int kEpiWarps = 16;     // epilogue: 4 per TMEM lane quarter
 constexpr int kLdWarps = 4;       // cp.async loaders
 constexpr int kLinThreads = 32 * (kEpiWarps + kLdWarps + 1);  // + the MMA issuer
 constexpr int kWbStride = 33;     // padded words per request row
@@ -90,34 +94,35 @@ struct LinArgs {
   uint32_t* task_counts;  // [R][C*32] popcount per 32-word group
 };
 
-// Warp-specialised: the loaders keep two A stages ahead (cp.async), the
-// issuer runs the tensor core into two TMEM buffers, the epilogue drains one
-// buffer while the other fills; full/empty mbarriers for both hand-offs.
+// Warp-specialised: the loaders keep two B stages ahead (cp.async), the
+// issuer runs the tensor core into two TMEM stages, the epilogue drains one
+// stage while the other fills; full/empty mbarriers for both hand-offs.
 __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int KC = a.D / 8;                        // 16-byte K-chunks per row
-  unsigned char* sb = smem;                      // [256 requests][D] core-matrix layout
-  unsigned char* sa[2];
-  sa[0] = sb + (size_t)kLinN * a.D * 2;
-  sa[1] = sa[0] + (size_t)kLinM * a.D * 2;
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sa[1] + (size_t)kLinM * a.D * 2);  // [256][33]
+  unsigned char* sa = smem;                      // [256 requests][D] core-matrix layout
+  unsigned char* sb[2];
+  sb[0] = sa + (size_t)kLinR * a.D * 2;          // [128 configurations][D], two stages
+  sb[1] = sb[0] + (size_t)kLinN * a.D * 2;
+  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sb[1] + (size_t)kLinN * a.D * 2);  // [256][33]
+  __shared__ __align__(16) float s_thr[kEpiWarps][64];  // per epilogue warp: its 64 columns
   __shared__ uint32_t s_tmem;
-  __shared__ __align__(8) uint64_t b_full, a_full[2], a_empty[2], t_full[2], t_empty[2];
+  __shared__ __align__(8) uint64_t a_full, b_full[2], b_empty[2], t_full[2], t_empty[2];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int r0 = blockIdx.y * kLinN;
-  const uint64_t cbase = a.begin + (uint64_t)blockIdx.x * (kLinM * kLinTiles);
+  const int r0 = blockIdx.y * kLinR;
+  const uint64_t cbase = a.begin + (uint64_t)blockIdx.x * (kLinN * kLinTiles);
   // tiles of this CTA that hold any configuration of [begin, end)
-  const int T = (int)min((uint64_t)kLinTiles, (a.end - cbase + kLinM - 1) / kLinM);
+  const int T = (int)min((uint64_t)kLinTiles, (a.end - cbase + kLinN - 1) / kLinN);
 
   if (wid == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&s_tmem)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&b_full, 32 * kLdWarps);
+    mbar_init(&a_full, 32 * kLdWarps);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&a_full[i], 32 * kLdWarps);
-      mbar_init(&a_empty[i], 1);
+      mbar_init(&b_full[i], 32 * kLdWarps);
+      mbar_init(&b_empty[i], 1);
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 32 * kEpiWarps);
     }
@@ -132,73 +137,83 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   if (wid >= kEpiWarps && wid < kEpiWarps + kLdWarps) {
     // ---------------------------------------------------------- loaders
     const int lt = tid - 32 * kEpiWarps;
-    for (int i = lt; i < kLinN * KC; i += kLd) {
+    for (int i = lt; i < kLinR * KC; i += kLd) {
       const int row = i / KC, kc = i - row * KC;
       const bool ok = r0 + row < a.R;
-      cp16(sb + cm_off(row, kc, KC), a.emb + (size_t)(ok ? r0 + row : 0) * KC + kc, ok);
+      cp16(sa + cm_off(row, kc, KC), a.emb + (size_t)(ok ? r0 + row : 0) * KC + kc, ok);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    mbar_arrive(&b_full);
+    mbar_arrive(&a_full);
     for (int t = 0; t < T; ++t) {
       const int s = t & 1;
-      mbar_wait(&a_empty[s], ((t >> 1) & 1) ^ 1);
-      const uint64_t c0 = cbase + (uint64_t)t * kLinM;
-      for (int i = lt; i < kLinM * KC; i += kLd) {
+      mbar_wait(&b_empty[s], ((t >> 1) & 1) ^ 1);
+      const uint64_t c0 = cbase + (uint64_t)t * kLinN;
+      for (int i = lt; i < kLinN * KC; i += kLd) {
         const int row = i / KC, kc = i - row * KC;
         const uint64_t c = c0 + row;
         const bool ok = c < a.end;
-        cp16(sa[s] + cm_off(row, kc, KC), a.heads + (ok ? c : 0) * KC + kc, ok);
+        cp16(sb[s] + cm_off(row, kc, KC), a.heads + (ok ? c : 0) * KC + kc, ok);
       }
       asm volatile("cp.async.wait_all;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&a_full[s]);
+      mbar_arrive(&b_full[s]);
     }
   } else if (wid == kEpiWarps + kLdWarps) {
     // ---------------------------------------------------------- MMA issue
     if (lane == 0) {
-      // bf16 x bf16 -> f32, K-major both, M 128, N 256
+      // bf16 x bf16 -> f32, K-major both, M 128, N 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLinN >> 3) << 17) |
                              ((uint32_t)(kLinM >> 4) << 24);
       const uint32_t lbo = 128, sbo = (uint32_t)KC * 128;
-      mbar_wait(&b_full, 0);
+      const uint32_t half = (uint32_t)kLinM * KC * 16;  // byte offset of request rows 128..255
+      mbar_wait(&a_full, 0);
       for (int t = 0; t < T; ++t) {
         const int s = t & 1;
-        mbar_wait(&a_full[s], (t >> 1) & 1);
+        mbar_wait(&b_full[s], (t >> 1) & 1);
         mbar_wait(&t_empty[s], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t acc = tmem + (uint32_t)(s * kLinN);
-        for (int ks = 0; ks < a.D / 16; ++ks) {
-          const uint64_t da = sdesc(su32(sa[s]) + ks * 256, lbo, sbo);
-          const uint64_t db = sdesc(su32(sb) + ks * 256, lbo, sbo);
-          const uint32_t accumulate = ks > 0 ? 1u : 0u;
-          asm volatile(
-              "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
-              "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
-              : "memory");
+        for (int hf = 0; hf < 2; ++hf) {
+          const uint32_t acc = tmem + (uint32_t)(s * 2 * kLinN + hf * kLinN);
+          for (int ks = 0; ks < a.D / 16; ++ks) {
+            const uint64_t da = sdesc(su32(sa) + hf * half + ks * 256, lbo, sbo);
+            const uint64_t db = sdesc(su32(sb[s]) + ks * 256, lbo, sbo);
+            const uint32_t accumulate = ks > 0 ? 1u : 0u;
+            asm volatile(
+                "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
+                "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
+                : "memory");
+          }
         }
-        umma_commit(&a_empty[s]);  // stage s may be refilled once these MMAs are done
-        umma_commit(&t_full[s]);   // and the accumulator is ready
+        umma_commit(&b_empty[s]);  // stage s may be refilled once these MMAs are done
+        umma_commit(&t_full[s]);   // and the accumulators are ready
       }
     }
   } else {
     // ---------------------------------------------------------- epilogue
-    // rows = configurations (lane = configuration in the warp's 32; warp w
-    // reads TMEM lane quarter w % 4), columns = requests (warp w takes the
-    // 64 columns (w / 4) * 64 ..); one ballot per column gives a word
-    const int q = wid & 3, h = wid >> 2;
-    constexpr int kCols = kLinN / (kEpiWarps / 4);
+    // TMEM lane = request (warp w reads lane quarter w % 4), columns =
+    // configurations: warp w takes request half (w / 8) and the 64 columns
+    // ((w / 4) & 1) * 64 .. of it; a thread's 32 columns make one word
+    const int q = wid & 3, hf = wid >> 3, ch = (wid >> 2) & 1;
+    const int row = hf * kLinM + q * 32 + lane;  // request row in the CTA
+    float* thr = s_thr[wid];
     for (int t = 0; t < T; ++t) {
       const int s = t & 1;
+      // thresholds of this warp's 64 configurations: acc + b > 0 <=> acc > -b
+      {
+        const uint64_t c = cbase + (uint64_t)t * kLinN + (uint64_t)(ch * 64 + lane);
+        thr[lane] = c < a.end ? -__ldg(a.bias + c) : INFINITY;
+        thr[32 + lane] = c + 32 < a.end ? -__ldg(a.bias + c + 32) : INFINITY;
+        __syncwarp();
+      }
       mbar_wait(&t_full[s], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t c = cbase + (uint64_t)t * kLinM + (uint64_t)(q * 32 + lane);
-      const float thr = c < a.end ? -__ldg(a.bias + c) : INFINITY;  // acc + b > 0 <=> acc > -b
-      const int widx = (t & 7) * 4 + q;  // word within the group
-      for (int c0 = h * kCols; c0 < (h + 1) * kCols; c0 += 32) {
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
         uint32_t v[32];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * kLinN + c0);
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) +
+                               (uint32_t)(s * 2 * kLinN + hf * kLinN + ch * 64 + k * 32);
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
@@ -209,25 +224,23 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
               "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c0 + 32 == (h + 1) * kCols) {  // this warp's part is drained
+        if (k == 1) {  // this warp's part of the stage is drained
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           mbar_arrive(&t_empty[s]);
         }
-        // lane = configuration row: bit j = verdict for request column j;
-        // a 32x32 bit transpose across the warp turns rows into the
-        // requests' words (lane j <- column j)
         uint32_t x = 0;
+        const float4* th = reinterpret_cast<const float4*>(thr + 32 * k);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) x |= (__uint_as_float(v[j]) > thr ? 1u : 0u) << j;
-#pragma unroll
-        for (int k = 16; k >= 1; k >>= 1) {
-          const uint32_t ml = k == 16 ? 0x0000FFFFu : k == 8 ? 0x00FF00FFu : k == 4 ? 0x0F0F0F0Fu
-                            : k == 2 ? 0x33333333u : 0x55555555u;
-          const uint32_t o = __shfl_xor_sync(0xffffffffu, x, k);
-          x = (lane & k) ? ((x & ~ml) | ((o & ~ml) >> k)) : ((x & ml) | ((o & ml) << k));
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const float4 tv = th[j4];  // broadcast
+          x |= (__uint_as_float(v[4 * j4 + 0]) > tv.x ? 1u : 0u) << (4 * j4 + 0);
+          x |= (__uint_as_float(v[4 * j4 + 1]) > tv.y ? 1u : 0u) << (4 * j4 + 1);
+          x |= (__uint_as_float(v[4 * j4 + 2]) > tv.z ? 1u : 0u) << (4 * j4 + 2);
+          x |= (__uint_as_float(v[4 * j4 + 3]) > tv.w ? 1u : 0u) << (4 * j4 + 3);
         }
-        wbuf[(c0 + lane) * kWbStride + widx] = x;
+        wbuf[row * kWbStride + (t & 7) * 4 + ch * 2 + k] = x;
       }
+      __syncwarp();  // thr is rewritten for the next tile
       if ((t & 7) == 7 || t + 1 == T) {
         // the group is complete: 256 request rows of 32 words, top forced,
         // tail masked; per-group counts for the scans
@@ -236,7 +249,7 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
         const uint64_t wi = (uint64_t)grp * 32 + lane;
         const uint64_t i0 = a.begin + wi * 32;
         const int nw = ((t & 7) + 1) * 4;  // words of the group written by the tiles
-        for (int rr = wid; rr < kLinN; rr += kEpiWarps) {
+        for (int rr = wid; rr < kLinR; rr += kEpiWarps) {
           const int r = r0 + rr;
           if (r >= a.R) break;
           uint32_t w = lane < nw ? wbuf[rr * kWbStride + lane] : 0u;
@@ -320,16 +333,16 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
     a.G = G;
     a.bitmap = bitmap;
     a.task_counts = (uint32_t*)ctx->chunk_counts.p;
-    const size_t smem = (size_t)(agb::kLinN + 2 * agb::kLinM) * heads->dim * 2 +
-                        (size_t)agb::kLinN * agb::kWbStride * 4;
+    const size_t smem = (size_t)(agb::kLinR + 2 * agb::kLinN) * heads->dim * 2 +
+                        (size_t)agb::kLinR * agb::kWbStride * 4;
     static bool attr = false;
     if (!attr) {
-      const int max_smem = (agb::kLinN + 2 * agb::kLinM) * 128 * 2 + agb::kLinN * agb::kWbStride * 4;
+      const int max_smem = (agb::kLinR + 2 * agb::kLinN) * 128 * 2 + agb::kLinR * agb::kWbStride * 4;
       AG_CUDA(cudaFuncSetAttribute(agb::k_linear_score, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
       attr = true;
     }
     const uint32_t per_cta = agb::kLinTiles / 8;  // groups per CTA
-    const dim3 grid((G + per_cta - 1) / per_cta, (R + agb::kLinN - 1) / agb::kLinN);
+    const dim3 grid((G + per_cta - 1) / per_cta, (R + agb::kLinR - 1) / agb::kLinR);
     {
       agb::Launch L(ctx, agb::K_LINEAR_SCORE);
       agb::k_linear_score<<<grid, agb::kLinThreads, smem, s>>>(a);
