@@ -38,7 +38,8 @@ constexpr int kLinR = 256;        // requests per CTA (two MMAs per K step)
 constexpr int kLinN = 128;        // configurations per tile (MMA N)
 constexpr int kLinTiles = 16;     // configuration tiles per CTA (2 groups of 1024)
 constexpr int kEpiWarps = 16;     // epilogue: 4 per TMEM lane quarter
-constexpr int kLdWarps = 4;       // cp.async loaders
+constexpr int kLdWarps = 8;       // cp.async loaders
+constexpr int kBStages = 3;       // configuration-tile stages in shared memory
 constexpr int kLinThreads = 32 * (kEpiWarps + kLdWarps + 1);  // + the MMA issuer
 constexpr int kWbStride = 33;     // padded words per request row
 
@@ -70,6 +71,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mb, uint32_t parity) {
         : "r"(su32(mb)), "r"(parity)
         : "memory");
 }
+// waiting roles that share a sub-partition with the MMA issuer back off, so
+// their spins do not take its issue slots
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mb, uint32_t parity) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(su32(mb)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(64);
+  }
+}
 __device__ __forceinline__ void umma_commit(uint64_t* mb) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mb))
                : "memory");
@@ -97,17 +112,21 @@ struct LinArgs {
 // Warp-specialised: the loaders keep two B stages ahead (cp.async), the
 // issuer runs the tensor core into two TMEM stages, the epilogue drains one
 // stage while the other fills; full/empty mbarriers for both hand-offs.
+// NKS = D / 16 MMA K steps per tile, unrolled (descriptors advance by a
+// constant: the issue loop is the tensor core's feed rate)
+template <int NKS>
 __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const int KC = a.D / 8;                        // 16-byte K-chunks per row
   unsigned char* sa = smem;                      // [256 requests][D] core-matrix layout
-  unsigned char* sb[2];
-  sb[0] = sa + (size_t)kLinR * a.D * 2;          // [128 configurations][D], two stages
-  sb[1] = sb[0] + (size_t)kLinN * a.D * 2;
-  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sb[1] + (size_t)kLinN * a.D * 2);  // [256][33]
-  __shared__ __align__(16) float s_thr[kEpiWarps][64];  // per epilogue warp: its 64 columns
+  unsigned char* sb[kBStages];                   // [128 configurations][D] per stage
+  sb[0] = sa + (size_t)kLinR * a.D * 2;
+  for (int i = 1; i < kBStages; ++i) sb[i] = sb[i - 1] + (size_t)kLinN * a.D * 2;
+  uint32_t* wbuf = reinterpret_cast<uint32_t*>(sb[kBStages - 1] + (size_t)kLinN * a.D * 2);  // [256][33]
+  // thresholds of every configuration of the CTA (acc + b > 0 <=> acc > -b)
+  __shared__ __align__(16) float s_thr[kLinN * kLinTiles];
   __shared__ uint32_t s_tmem;
-  __shared__ __align__(8) uint64_t a_full, b_full[2], b_empty[2], t_full[2], t_empty[2];
+  __shared__ __align__(8) uint64_t a_full, b_full[kBStages], b_empty[kBStages], t_full[2], t_empty[2];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int r0 = blockIdx.y * kLinR;
   const uint64_t cbase = a.begin + (uint64_t)blockIdx.x * (kLinN * kLinTiles);
@@ -120,9 +139,11 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   }
   if (tid == 0) {
     mbar_init(&a_full, 32 * kLdWarps);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kBStages; ++i) {
       mbar_init(&b_full[i], 32 * kLdWarps);
       mbar_init(&b_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&t_full[i], 1);
       mbar_init(&t_empty[i], 32 * kEpiWarps);
     }
@@ -137,28 +158,39 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
   if (wid >= kEpiWarps && wid < kEpiWarps + kLdWarps) {
     // ---------------------------------------------------------- loaders
     const int lt = tid - 32 * kEpiWarps;
+    // thread i fills row i % 8 of core matrix i / 8: a warp writes 512
+    // contiguous bytes of shared memory (conflict-free) and reads 64-byte
+    // runs of 8 rows
     for (int i = lt; i < kLinR * KC; i += kLd) {
-      const int row = i / KC, kc = i - row * KC;
+      const int cmi = i >> 3, g = cmi / KC, kc = cmi - g * KC, row = g * 8 + (i & 7);
       const bool ok = r0 + row < a.R;
-      cp16(sa + cm_off(row, kc, KC), a.emb + (size_t)(ok ? r0 + row : 0) * KC + kc, ok);
+      cp16(sa + cmi * 128 + (i & 7) * 16, a.emb + (size_t)(ok ? r0 + row : 0) * KC + kc, ok);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_arrive(&a_full);
+    // two tiles' copies in flight per thread: tile t is issued before tile
+    // t - 1 is waited for and published
     for (int t = 0; t < T; ++t) {
-      const int s = t & 1;
-      mbar_wait(&b_empty[s], ((t >> 1) & 1) ^ 1);
+      const int s = t % kBStages;
+      mbar_wait_sleep(&b_empty[s], ((t / kBStages) & 1) ^ 1);
       const uint64_t c0 = cbase + (uint64_t)t * kLinN;
       for (int i = lt; i < kLinN * KC; i += kLd) {
-        const int row = i / KC, kc = i - row * KC;
-        const uint64_t c = c0 + row;
+        const int cmi = i >> 3, g = cmi / KC, kc = cmi - g * KC;
+        const uint64_t c = c0 + (uint64_t)(g * 8 + (i & 7));
         const bool ok = c < a.end;
-        cp16(sb[s] + cm_off(row, kc, KC), a.heads + (ok ? c : 0) * KC + kc, ok);
+        cp16(sb[s] + cmi * 128 + (i & 7) * 16, a.heads + (ok ? c : 0) * KC + kc, ok);
       }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&b_full[s]);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (t > 0) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&b_full[(t - 1) % kBStages]);
+      }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (T > 0) mbar_arrive(&b_full[(T - 1) % kBStages]);
   } else if (wid == kEpiWarps + kLdWarps) {
     // ---------------------------------------------------------- MMA issue
     if (lane == 0) {
@@ -167,26 +199,31 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
                              ((uint32_t)(kLinM >> 4) << 24);
       const uint32_t lbo = 128, sbo = (uint32_t)KC * 128;
       const uint32_t half = (uint32_t)kLinM * KC * 16;  // byte offset of request rows 128..255
+      // descriptors precomputed; K step ks adds 256 bytes = 16 to the
+      // start-address field (addresses stay below 256 KB: no carry out)
+      const uint64_t da0 = sdesc(su32(sa), lbo, sbo), da1 = sdesc(su32(sa) + half, lbo, sbo);
+      const uint64_t db0 = sdesc(su32(sb[0]), lbo, sbo);
+      const uint64_t b_stage = ((uint64_t)kLinN * KC * 16) >> 4;
       mbar_wait(&a_full, 0);
       for (int t = 0; t < T; ++t) {
-        const int s = t & 1;
-        mbar_wait(&b_full[s], (t >> 1) & 1);
+        const int s = t & 1, bs = t % kBStages;
+        mbar_wait(&b_full[bs], (t / kBStages) & 1);
         mbar_wait(&t_empty[s], ((t >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t db = db0 + (uint64_t)bs * b_stage;
+#pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
           const uint32_t acc = tmem + (uint32_t)(s * 2 * kLinN + hf * kLinN);
-          for (int ks = 0; ks < a.D / 16; ++ks) {
-            const uint64_t da = sdesc(su32(sa) + hf * half + ks * 256, lbo, sbo);
-            const uint64_t db = sdesc(su32(sb[s]) + ks * 256, lbo, sbo);
-            const uint32_t accumulate = ks > 0 ? 1u : 0u;
+          const uint64_t da = hf ? da1 : da0;
+#pragma unroll
+          for (int ks = 0; ks < NKS; ++ks) {
             asm volatile(
                 "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
-                "l"(da), "l"(db), "r"(idesc), "r"(accumulate)
-                : "memory");
+                "l"(da + 16u * ks), "l"(db + 16u * ks), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
           }
         }
-        umma_commit(&b_empty[s]);  // stage s may be refilled once these MMAs are done
+        umma_commit(&b_empty[bs]);  // stage bs may be refilled once these MMAs are done
         umma_commit(&t_full[s]);   // and the accumulators are ready
       }
     }
@@ -197,17 +234,15 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
     // ((w / 4) & 1) * 64 .. of it; a thread's 32 columns make one word
     const int q = wid & 3, hf = wid >> 3, ch = (wid >> 2) & 1;
     const int row = hf * kLinM + q * 32 + lane;  // request row in the CTA
-    float* thr = s_thr[wid];
+    for (int i = tid; i < kLinN * kLinTiles; i += 32 * kEpiWarps) {
+      const uint64_t c = cbase + (uint64_t)i;
+      s_thr[i] = c < a.end ? -__ldg(a.bias + c) : INFINITY;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     for (int t = 0; t < T; ++t) {
       const int s = t & 1;
-      // thresholds of this warp's 64 configurations: acc + b > 0 <=> acc > -b
-      {
-        const uint64_t c = cbase + (uint64_t)t * kLinN + (uint64_t)(ch * 64 + lane);
-        thr[lane] = c < a.end ? -__ldg(a.bias + c) : INFINITY;
-        thr[32 + lane] = c + 32 < a.end ? -__ldg(a.bias + c + 32) : INFINITY;
-        __syncwarp();
-      }
-      mbar_wait(&t_full[s], (t >> 1) & 1);
+      const float* thr = s_thr + t * kLinN + ch * 64;
+      mbar_wait_sleep(&t_full[s], (t >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
@@ -240,7 +275,6 @@ __global__ void __launch_bounds__(kLinThreads, 1) k_linear_score(LinArgs a) {
         }
         wbuf[row * kWbStride + (t & 7) * 4 + ch * 2 + k] = x;
       }
-      __syncwarp();  // thr is rewritten for the next tile
       if ((t & 7) == 7 || t + 1 == T) {
         // the group is complete: 256 request rows of 32 words, top forced,
         // tail masked; per-group counts for the scans
@@ -333,19 +367,25 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
     a.G = G;
     a.bitmap = bitmap;
     a.task_counts = (uint32_t*)ctx->chunk_counts.p;
-    const size_t smem = (size_t)(agb::kLinR + 2 * agb::kLinN) * heads->dim * 2 +
+    const size_t smem = (size_t)(agb::kLinR + agb::kBStages * agb::kLinN) * heads->dim * 2 +
                         (size_t)agb::kLinR * agb::kWbStride * 4;
+    typedef void (*lin_fn)(agb::LinArgs);
+    static const lin_fn fns[8] = {agb::k_linear_score<1>, agb::k_linear_score<2>, agb::k_linear_score<3>,
+                                  agb::k_linear_score<4>, agb::k_linear_score<5>, agb::k_linear_score<6>,
+                                  agb::k_linear_score<7>, agb::k_linear_score<8>};
+    const lin_fn fn = fns[heads->dim / 16 - 1];
     static bool attr = false;
     if (!attr) {
-      const int max_smem = (agb::kLinR + 2 * agb::kLinN) * 128 * 2 + agb::kLinR * agb::kWbStride * 4;
-      AG_CUDA(cudaFuncSetAttribute(agb::k_linear_score, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+      const int max_smem = (agb::kLinR + agb::kBStages * agb::kLinN) * 128 * 2 + agb::kLinR * agb::kWbStride * 4;
+      for (int i = 0; i < 8; ++i)
+        AG_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
       attr = true;
     }
     const uint32_t per_cta = agb::kLinTiles / 8;  // groups per CTA
     const dim3 grid((G + per_cta - 1) / per_cta, (R + agb::kLinR - 1) / agb::kLinR);
     {
       agb::Launch L(ctx, agb::K_LINEAR_SCORE);
-      agb::k_linear_score<<<grid, agb::kLinThreads, smem, s>>>(a);
+      fn<<<grid, agb::kLinThreads, smem, s>>>(a);
     }
     AG_CUDA(cudaGetLastError());
   }
