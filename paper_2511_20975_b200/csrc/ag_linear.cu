@@ -46,10 +46,9 @@ constexpr int kWbStride = 33;     // padded words per request row
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // canonical K-major, no swizzle: core matrix = 8 rows x 16 B; K-chunks of a
-// row group 128 B apart (LBO); row groups KC * 128 B apart (SBO)
-__device__ __forceinline__ uint32_t cm_off(int row, int kc, int KC) {
-  return (uint32_t)(((row >> 3) * KC + kc) * 128 + (row & 7) * 16);
-}
+// row group 128 B apart (LBO); row groups KC * 128 B apart (SBO).  Core
+// matrix cmi = (row / 8) * KC + kc starts at byte cmi * 128 (the loaders
+// fill them in that order).
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
