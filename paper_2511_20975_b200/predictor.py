@@ -86,5 +86,8 @@ class ConfigPredictor:
         return res
 
     def __del__(self):
-        _capi.release("ag_predictor_destroy", getattr(self, "_h", None))
+        try:  # module globals may already be gone at interpreter shutdown
+            _capi.release("ag_predictor_destroy", getattr(self, "_h", None))
+        except Exception:  # noqa: BLE001
+            pass
         self._h = None

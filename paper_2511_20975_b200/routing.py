@@ -84,7 +84,10 @@ class ConfigSpace:
         return self.size - 1
 
     def __del__(self):
-        _capi.release("ag_space_destroy", getattr(self, "_h", None))
+        try:  # module globals may already be gone at interpreter shutdown
+            _capi.release("ag_space_destroy", getattr(self, "_h", None))
+        except Exception:  # noqa: BLE001
+            pass
         self._h = None
 
 
@@ -340,7 +343,10 @@ class Device:
         return RouteResult(counts, offsets, indices[: total.value], None)
 
     def __del__(self):
-        _capi.release("ag_ctx_destroy", getattr(self, "_h", None))
+        try:  # module globals may already be gone at interpreter shutdown
+            _capi.release("ag_ctx_destroy", getattr(self, "_h", None))
+        except Exception:  # noqa: BLE001
+            pass
         self._h = None
 
 

@@ -182,7 +182,10 @@ class SchedSession:
         return out[: n.value]
 
     def __del__(self):
-        _capi.release("ag_sched_destroy", getattr(self, "_h", None))
+        try:  # module globals may already be gone at interpreter shutdown
+            _capi.release("ag_sched_destroy", getattr(self, "_h", None))
+        except Exception:  # noqa: BLE001
+            pass
         self._h = None
 
 
