@@ -617,6 +617,11 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   }
   wstatus = __shfl_sync(kFull, wstatus, 0);
   __syncwarp();
+  // occupancy of state w, engine e in lane (w << lgE) + e when every state's
+  // row fits the warp (B * E padded <= 32); shared-memory rows otherwise
+  const bool regocc = (B << lgE) <= 32;
+  const int ow = lane >> lgE, oe = lane & ((1 << lgE) - 1);
+  int occ_r = (ow == 0 && oe < E) ? A.eng.occ[oe] : 0;
   int cur = 0, nst = 1, nnodes = 0;
   unsigned long long explored = 1;
   long long pi = 0;  // next pair position not yet accounted for
@@ -981,12 +986,23 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     if (nnodes + __popc(nb) > A.max_nodes) wstatus = AG_ERR_INTERNAL + 300;  // history overflow (uniform)
     const int c_mdl = mknode ? e_model[c_eng] : 0;
     const uint64_t mykey = mknode ? key_base | (uint64_t)(uint32_t)c_mdl : kEnd;
-    // occupancy rows of the new states: lane (w, e) copies engine e of state w
-    for (int i0 = 0; i0 < (npick << lgE); i0 += 32) {
-      const int i = i0 + lane, w = min(i >> lgE, 31), e = i & ((1 << lgE) - 1);
-      const int pw = __shfl_sync(kFull, c_par, w);
-      const int ew = __shfl_sync(kFull, c_eng, w);
-      if (w < npick && e < E) s_occ[nxt][w][e] = s_occ[cur][pw][e] + (e == ew ? 1 : 0);
+    // occupancy rows of the new states: lane (w, e) takes engine e of the
+    // parent of state w, plus one on the adopted engine; p_occ = the parent's
+    // occupancy of the adopted engine (for state w's free mask)
+    int p_occ = 0;
+    if (regocc) {
+      p_occ = __shfl_sync(kFull, occ_r, (c_par << lgE) + (mknode ? c_eng : 0));
+      const int pw = __shfl_sync(kFull, c_par, ow);
+      const int ew = __shfl_sync(kFull, c_eng, ow);
+      occ_r = __shfl_sync(kFull, occ_r, (pw << lgE) + oe) + (oe == ew ? 1 : 0);
+    } else {
+      if (mine && mknode) p_occ = s_occ[cur][c_par][c_eng];
+      for (int i0 = 0; i0 < (npick << lgE); i0 += 32) {
+        const int i = i0 + lane, w = min(i >> lgE, 31), e = i & ((1 << lgE) - 1);
+        const int pw = __shfl_sync(kFull, c_par, w);
+        const int ew = __shfl_sync(kFull, c_eng, w);
+        if (w < npick && e < E) s_occ[nxt][w][e] = s_occ[cur][pw][e] + (e == ew ? 1 : 0);
+      }
     }
     if (mine) {
       st_u = c_u;
@@ -996,7 +1012,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       st_ns = c_ns;
       st_fm = p_fm;
       if (mknode) {
-        if (s_occ[cur][c_par][c_eng] + 1 >= e_slots[c_eng]) st_fm &= ~(1u << c_eng);
+        if (p_occ + 1 >= e_slots[c_eng]) st_fm &= ~(1u << c_eng);
         const int id = nnodes + __popc(nb & lt);
         if (!wstatus) {
           Node nd;
@@ -1037,6 +1053,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     nst = npick;
     AG_PHASE_TICK(3);
   }
+  if (regocc && ow < nst && oe < E) s_occ[cur][ow][oe] = occ_r;
+  __syncwarp();
   // producers stop at their next chunk boundary
   if (lane == 0) *(volatile unsigned*)&s_walk_done = 1u;
   if (lane == 0 && A.timing) {
