@@ -109,6 +109,11 @@ struct ChainBuilder {  // predictor.cpp:28-99
 __device__ __forceinline__ bool bit_get(const uint32_t* b, uint32_t i) {
   return (b[i >> 5] >> (i & 31)) & 1u;
 }
+// the known / value bitsets interleaved word by word: one 8-byte load gives
+// both bits of a rung
+__device__ __forceinline__ uint2 kv_word(const uint32_t* kv, uint32_t u) {
+  return reinterpret_cast<const uint2*>(kv)[u >> 5];
+}
 
 struct PredictArgs {
   SpaceDev sp;
@@ -167,14 +172,13 @@ __device__ bool verdict(const PredictArgs& a, int r, uint32_t idx, uint64_t P) {
 constexpr int kPredWarps = 4;
 
 __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
-  extern __shared__ uint32_t smem[];
+  extern __shared__ __align__(16) uint32_t smem[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int r = blockIdx.x * kPredWarps + wid;
   if (r >= a.R) return;
   uint32_t* base = a.smem_bits ? smem + (size_t)wid * 4 * a.words
                                : a.gscratch + (size_t)r * 4 * a.words;
-  uint32_t* known = base;
-  uint32_t* value = base + a.words;
+  uint32_t* kv = base;  // known / value interleaved, 2 * words
   uint32_t* cand = base + 2 * a.words;
   uint32_t* kept = base + 3 * a.words;
   for (int i = lane; i < 4 * a.words; i += 32) base[i] = 0;
@@ -202,8 +206,9 @@ __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
       bool ct = false, cf = false;
       if (i < len) {
         const uint32_t u = __ldg(ch + i);
-        const bool k = u == a.uid_top || bit_get(known, u);
-        const bool v = u == a.uid_top || bit_get(value, u);
+        const uint2 w = kv_word(kv, u);
+        const bool k = u == a.uid_top || ((w.x >> (u & 31)) & 1u);
+        const bool v = u == a.uid_top || ((w.y >> (u & 31)) & 1u);
         ct = k && v;
         cf = k && !v;
       }
@@ -220,11 +225,12 @@ __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
       while (lo < hi) {
         const int mid = lo + (hi - lo) / 2;
         const uint32_t u = __ldg(ch + mid);
+        const uint2 w = kv_word(kv, u);
         bool v;
         if (u == a.uid_top) {
           v = true;
-        } else if (bit_get(known, u)) {
-          v = bit_get(value, u);
+        } else if ((w.x >> (u & 31)) & 1u) {
+          v = (w.y >> (u & 31)) & 1u;
         } else if (router_time + lat > budget) {
           truncated = true;
           aborted = true;
@@ -234,8 +240,8 @@ __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
           router_time += lat;
           ++search_evals;
           if (lane == 0) {
-            known[u >> 5] |= 1u << (u & 31);
-            if (v) value[u >> 5] |= 1u << (u & 31);
+            kv[2 * (u >> 5)] |= 1u << (u & 31);
+            if (v) kv[2 * (u >> 5) + 1] |= 1u << (u & 31);
           }
           __syncwarp();
         }
@@ -261,8 +267,9 @@ __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
     if (j < a.U) {
       u = __ldg(a.uid_by_cost + j);
       is_cand = bit_get(cand, u);
-      is_known = bit_get(known, u);
-      val = bit_get(value, u);
+      const uint2 w = kv_word(kv, u);
+      is_known = (w.x >> (u & 31)) & 1u;
+      val = (w.y >> (u & 31)) & 1u;
     }
     const uint32_t need = __ballot_sync(0xffffffffu, is_cand && !is_known);
     uint32_t charged = 0;
@@ -289,8 +296,8 @@ __global__ void __launch_bounds__(kPredWarps * 32) k_predict(PredictArgs a) {
         keep = val;
       } else if ((charged >> lane) & 1u) {
         keep = verdict(a, r, __ldg(a.uniq_index + u), P);
-        atomicOr(known + (u >> 5), 1u << (u & 31));
-        if (keep) atomicOr(value + (u >> 5), 1u << (u & 31));
+        atomicOr(kv + 2 * (u >> 5), 1u << (u & 31));
+        if (keep) atomicOr(kv + 2 * (u >> 5) + 1, 1u << (u & 31));
       }
     }
     if (keep) atomicOr(kept + (u >> 5), 1u << (u & 31));
