@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
   unsigned char* sb = sa + 2 * kMaxKB * kBox;                 // [stage][kb] boxes
   uint32_t* wbuf = reinterpret_cast<uint32_t*>(sb + kBStages * kMaxKB * kBox);  // [256][33]
   float* s_thr = reinterpret_cast<float*>(wbuf + kLinR * kWbStride);            // [1024]
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_thr + kLinN * kGroupTiles);   // [256][2]
   __shared__ uint32_t s_tmem;
   __shared__ __align__(8) uint64_t a_full, a_empty, b_full[kBStages], b_empty[kBStages], t_full[2], t_empty[2];
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     // ((w / 4) & 1) * 64 .. of a tile; a thread's 32 columns make one word
     const int q = wid & 3, hf = wid >> 3, ch = (wid >> 2) & 1;
     const int row = hf * kLinM + q * 32 + lane;  // request row in the block
-    uint32_t gt = 0;
+    uint32_t gt = 0, cnt = 0;
     for (uint32_t it = it0; it < it1; ++it) {
       const uint32_t rb = it / a.G, grp = it - rb * a.G;
       const int T = item_tiles(grp);
@@ -304,28 +305,31 @@ __global__ void __launch_bounds__(kLinThreads, 1)
             x = __funnelshift_l(y1, x, 1);
             x = __funnelshift_l(y0, x, 1);
           }
+          // tail mask and forced top (warp-uniform: the word index is)
+          const uint64_t wi = (uint64_t)grp * 32 + t * 4 + ch * 2 + k, i0 = a.begin + wi * 32;
+          if (wi >= a.W) {
+            x = 0;
+          } else {
+            if (a.end - i0 < 32) x &= (1u << (uint32_t)(a.end - i0)) - 1u;
+            if ((a.flags & AG_FORCE_TOP) && a.top >= i0 && a.top < i0 + 32) x |= 1u << (uint32_t)(a.top - i0);
+          }
           wbuf[row * kWbStride + t * 4 + ch * 2 + k] = x;
+          cnt += __popc(x);
         }
       }
-      // the group is complete: 256 request rows of 32 words, top forced,
-      // tail masked; per-group counts for the scans
+      // the group is complete: 256 request rows of 32 words written out
+      // coalesced (a warp per row), per-group counts for the scans
+      s_cnt[row * 2 + ch] = cnt;
+      cnt = 0;
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
       const uint64_t wi = (uint64_t)grp * 32 + lane;
-      const uint64_t i0 = a.begin + wi * 32;
-      const int nw = T * 4;  // words of the group written by the tiles
-      for (int rr = wid; rr < kLinR; rr += kEpiWarps) {
-        const int r = (int)(rb * kLinR) + rr;
-        if (r >= a.R) break;
-        uint32_t w = lane < nw ? wbuf[rr * kWbStride + lane] : 0u;
-        if (wi >= a.W) w = 0;
-        else if (a.end - i0 < 32) w &= (1u << (uint32_t)(a.end - i0)) - 1u;
-        if ((a.flags & AG_FORCE_TOP) && wi < a.W && a.top >= i0 && a.top < i0 + 32) w |= 1u << (uint32_t)(a.top - i0);
-        if (wi < a.W) a.bitmap[(size_t)r * a.W + wi] = w;
-        uint32_t cnt = __popc(w);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if (lane == 0 && grp < a.G) a.task_counts[(size_t)r * a.C * 32 + grp] = cnt;
+      if (lane < T * 4 && wi < a.W) {
+        const int nr = min(kLinR, a.R - (int)(rb * kLinR));
+        uint32_t* dst = a.bitmap + (size_t)rb * kLinR * a.W + wi;
+        for (int rr = wid; rr < nr; rr += kEpiWarps) dst[(size_t)rr * a.W] = wbuf[rr * kWbStride + lane];
       }
+      if (tid < kLinR && (int)(rb * kLinR) + tid < a.R && grp < a.G)
+        a.task_counts[((size_t)rb * kLinR + tid) * a.C * 32 + grp] = s_cnt[2 * tid] + s_cnt[2 * tid + 1];
       asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory");
     }
   }
@@ -427,7 +431,8 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
     a.task_counts = (uint32_t*)ctx->chunk_counts.p;
     // A (two halves) + B stages + word buffer + thresholds + alignment slack
     const size_t smem = (size_t)(2 + agb::kBStages) * agb::kMaxKB * agb::kBox +
-                        (size_t)agb::kLinR * agb::kWbStride * 4 + agb::kLinN * agb::kGroupTiles * 4 + 1024;
+                        (size_t)agb::kLinR * agb::kWbStride * 4 + agb::kLinN * agb::kGroupTiles * 4 +
+                        agb::kLinR * 2 * 4 + 1024;
     typedef void (*lin_fn)(const CUtensorMap, const CUtensorMap, agb::LinArgs);
     static const lin_fn fns[8] = {agb::k_linear_score<1>, agb::k_linear_score<2>, agb::k_linear_score<3>,
                                   agb::k_linear_score<4>, agb::k_linear_score<5>, agb::k_linear_score<6>,
