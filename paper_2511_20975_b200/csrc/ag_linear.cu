@@ -251,6 +251,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       const uint32_t rb = it / a.G, grp = it - rb * a.G;
       const int T = item_tiles(grp);
       const uint64_t cb = a.begin + (uint64_t)grp * (kLinN * kGroupTiles);
+      // an item needs word masks only at the end of the range or around top
+      const bool edge = cb + kLinN * kGroupTiles > a.end ||
+                        ((a.flags & AG_FORCE_TOP) && a.top >= cb && a.top < cb + kLinN * kGroupTiles);
       // thresholds of the item (acc + b > 0 <=> acc > -b; -0 made +0, tail +inf)
       for (int i = tid; i < kLinN * kGroupTiles; i += 32 * kEpiWarps) {
         const uint64_t c = cb + (uint64_t)i;
@@ -307,11 +310,13 @@ __global__ void __launch_bounds__(kLinThreads, 1)
           }
           // tail mask and forced top (warp-uniform: the word index is)
           const uint64_t wi = (uint64_t)grp * 32 + t * 4 + ch * 2 + k, i0 = a.begin + wi * 32;
-          if (wi >= a.W) {
-            x = 0;
-          } else {
-            if (a.end - i0 < 32) x &= (1u << (uint32_t)(a.end - i0)) - 1u;
-            if ((a.flags & AG_FORCE_TOP) && a.top >= i0 && a.top < i0 + 32) x |= 1u << (uint32_t)(a.top - i0);
+          if (edge) {
+            if (wi >= a.W) {
+              x = 0;
+            } else {
+              if (a.end - i0 < 32) x &= (1u << (uint32_t)(a.end - i0)) - 1u;
+              if ((a.flags & AG_FORCE_TOP) && a.top >= i0 && a.top < i0 + 32) x |= 1u << (uint32_t)(a.top - i0);
+            }
           }
           wbuf[row * kWbStride + t * 4 + ch * 2 + k] = x;
           cnt += __popc(x);
