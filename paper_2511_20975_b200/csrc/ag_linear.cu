@@ -39,6 +39,9 @@
 namespace agb {
 namespace {
 
+#ifndef AG_LIN_EXP
+#define AG_LIN_EXP 0  // diagnostics: 1 = no threshold work, 2 = no TMEM loads either, 3 = spinning waits, 4 = B tiles loaded once (stale)
+#endif
 constexpr int kLinM = 128;        // requests per MMA (one TMEM lane each)
 constexpr int kLinR = 256;        // requests per work item (two MMAs per K step)
 constexpr int kLinN = 128;        // configurations per tile (MMA N)
@@ -97,6 +100,12 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* mb, uint32_t parity) {
 __device__ __forceinline__ void umma_commit(uint64_t* mb) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mb))
                : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* mb) {
+  asm volatile(
+      "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0]; }" ::"r"(su32(mb))
+      : "memory");
 }
 // one 64-element x 128-row box of a 2-D bf16 tensor map into shared memory
 __device__ __forceinline__ void tma_box(void* dst, const CUtensorMap* map, int k0, int row, uint64_t* mb) {
@@ -190,6 +199,12 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         for (int t = 0; t < T; ++t, ++gt) {
           const int s = gt % kBStages;
           mbar_wait(&b_empty[s], ((gt / kBStages) & 1) ^ 1);
+#if AG_LIN_EXP == 4 || AG_LIN_EXP == 9
+          if (gt >= kBStages) {
+            mbar_arrive(&b_full[s]);
+            continue;
+          }
+#endif
           mbar_expect_tx(&b_full[s], a.KB * kBox);
           for (int kb = 0; kb < a.KB; ++kb)
             tma_box(sb + (s * kMaxKB + kb) * kBox, &head_map, kb * 64, (int)(cb + (uint64_t)t * kLinN), &b_full[s]);
@@ -198,7 +213,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
     }
   } else if (wid == kEpiWarps + 1) {
     // ---------------------------------------------------------- MMA issue
-    if (lane == 0) {
+    {  // the whole warp runs the loop (uniform descriptors); one elected lane issues
       // bf16 x bf16 -> f32, K-major both, M 128, N 128
       const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kLinN >> 3) << 17) |
                              ((uint32_t)(kLinM >> 4) << 24);
@@ -215,28 +230,28 @@ __global__ void __launch_bounds__(kLinThreads, 1)
         for (int t = 0; t < T; ++t, ++gt) {
           const int ts = gt & 1, bs = gt % kBStages;
           mbar_wait(&b_full[bs], (gt / kBStages) & 1);
-          mbar_wait(&t_empty[ts], ((gt >> 1) & 1) ^ 1);
+          if (AG_LIN_EXP != 10) mbar_wait(&t_empty[ts], ((gt >> 1) & 1) ^ 1);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint64_t db = db0 + (uint64_t)((bs * kMaxKB * kBox) >> 4);
 #pragma unroll
-          for (int hf = 0; hf < 2; ++hf) {
+          for (int hf = 0; hf < (AG_LIN_EXP == 5 ? 1 : 2); ++hf) {
             const uint32_t acc = tmem + (uint32_t)(ts * 2 * kLinN + hf * kLinN);
             const uint64_t da = da0 + (uint64_t)((hf * kMaxKB * kBox) >> 4);
 #pragma unroll
-            for (int ks = 0; ks < NKS; ++ks) {
+            for (int ks = 0; ks < (AG_LIN_EXP == 6 ? NKS / 2 : NKS); ++ks) {
               // K step ks: box ks / 4, 32 bytes per step inside the atom
               const uint64_t off = (uint64_t)(((ks >> 2) * kBox + (ks & 3) * 32) >> 4);
               asm volatile(
-                  "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
+                  "{ .reg .pred p, e; elect.sync _|e, 0xffffffff; setp.ne.b32 p, %4, 0;\n"
+                  "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(acc),
                   "l"(da + off), "l"(db + off), "r"(idesc), "r"(ks > 0 ? 1u : 0u));
             }
           }
-          umma_commit(&b_empty[bs]);  // stage bs may be refilled once these MMAs are done
-          umma_commit(&t_full[ts]);   // and the accumulators are ready
+          umma_commit_elect(&b_empty[bs]);  // stage bs may be refilled once these MMAs are done
+          umma_commit_elect(&t_full[ts]);   // and the accumulators are ready
         }
         // A may be replaced once every MMA of this request block is done
-        if (it + 1 == it1 || (it + 1) / a.G != rb) umma_commit(&a_empty);
+        if (it + 1 == it1 || (it + 1) / a.G != rb) umma_commit_elect(&a_empty);
       }
     }
   } else {
@@ -263,10 +278,17 @@ __global__ void __launch_bounds__(kLinThreads, 1)
       for (int t = 0; t < T; ++t, ++gt) {
         const int ts = gt & 1;
         const float4* th = reinterpret_cast<const float4*>(s_thr + t * kLinN + ch * 64);
+#if AG_LIN_EXP == 3
+        mbar_wait(&t_full[ts], (gt >> 1) & 1);
+#else
         mbar_wait_sleep(&t_full[ts], (gt >> 1) & 1);
+#endif
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         uint32_t v[64];
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ts * 2 * kLinN + hf * kLinN + ch * 64);
+#if AG_LIN_EXP == 2 || AG_LIN_EXP == 5 || AG_LIN_EXP == 6 || AG_LIN_EXP >= 9
+        for (int k = 0; k < 64; ++k) v[k] = 0;
+#else
 #pragma unroll
         for (int k = 0; k < 2; ++k)
           asm volatile(
@@ -282,6 +304,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
                 "=r"(v[32 * k + 28]), "=r"(v[32 * k + 29]), "=r"(v[32 * k + 30]), "=r"(v[32 * k + 31])
               : "r"(taddr + 32u * k));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#endif
         // this warp's part of the stage is drained
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -289,6 +312,9 @@ __global__ void __launch_bounds__(kLinThreads, 1)
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
           uint32_t x = 0;
+#if AG_LIN_EXP == 1 || AG_LIN_EXP == 2 || AG_LIN_EXP == 5 || AG_LIN_EXP == 6 || AG_LIN_EXP >= 9
+          x = v[32 * k] ^ v[32 * k + 31];
+#else
           // highest configuration first: after 32 shifts configuration j sits at bit j
 #pragma unroll
           for (int j4 = 7; j4 >= 0; --j4) {
@@ -308,6 +334,7 @@ __global__ void __launch_bounds__(kLinThreads, 1)
             x = __funnelshift_l(y1, x, 1);
             x = __funnelshift_l(y0, x, 1);
           }
+#endif
           // tail mask and forced top (warp-uniform: the word index is)
           const uint64_t wi = (uint64_t)grp * 32 + t * 4 + ch * 2 + k, i0 = a.begin + wi * 32;
           if (edge) {
