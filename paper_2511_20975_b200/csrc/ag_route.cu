@@ -706,16 +706,17 @@ __global__ void __launch_bounds__(1024)
 }
 
 // K2b: exclusive scan over requests -> offsets[R+1], overflow flag.  One
-// block, tiles of 4 x 1024 counts: loaded and stored coalesced through shared
-// memory (a single SM's L1 is the limit: per-thread contiguous runs would
-// cost one sector request per element), each thread scanning 4 contiguous
-// counts of the tile; the tile total carries to the next tile.
-constexpr int kReqPer = 4;
-
+// block, tiles of PER x 1024 counts (PER picked so a batch is one tile up to
+// 24k requests: every load of the batch is in flight at once, then one
+// scan): loaded and stored coalesced through shared memory (a single SM's L1
+// is the limit: per-thread contiguous runs would cost one sector request per
+// element), each thread scanning PER contiguous counts of the tile; the tile
+// total carries to the next tile.
+template <int kReqPer>
 __global__ void __launch_bounds__(1024)
     k_request_scan(const uint64_t* __restrict__ counts, uint64_t* __restrict__ offsets, int R,
                    uint64_t capacity, uint32_t* __restrict__ overflow) {
-  __shared__ uint64_t s_t[kReqPer * 1024];
+  extern __shared__ uint64_t s_t[];  // [kReqPer * 1024]
   __shared__ uint64_t warp_sums[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t carry = 0;
@@ -727,12 +728,9 @@ __global__ void __launch_bounds__(1024)
       s_t[i] = i < n ? __ldg(counts + t0 + i) : 0ull;
     }
     __syncthreads();
-    uint64_t v[kReqPer], local = 0;
+    uint64_t local = 0;
 #pragma unroll
-    for (int u = 0; u < kReqPer; ++u) {
-      v[u] = s_t[threadIdx.x * kReqPer + u];
-      local += v[u];
-    }
+    for (int u = 0; u < kReqPer; ++u) local += s_t[threadIdx.x * kReqPer + u];
     uint64_t x = local;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -755,8 +753,9 @@ __global__ void __launch_bounds__(1024)
     uint64_t run = carry + warp_sums[wid] + x - local;
 #pragma unroll
     for (int u = 0; u < kReqPer; ++u) {
+      const uint64_t c = s_t[threadIdx.x * kReqPer + u];
       s_t[threadIdx.x * kReqPer + u] = run;
-      run += v[u];
+      run += c;
     }
     __syncthreads();  // tile offsets staged; every warp prefix read
 #pragma unroll
@@ -773,6 +772,25 @@ __global__ void __launch_bounds__(1024)
     offsets[R] = carry;
     if (overflow) *overflow = carry > capacity ? 1u : 0u;
   }
+}
+
+cudaError_t launch_request_scan(cudaStream_t s, const uint64_t* counts, uint64_t* offsets, int R, uint64_t capacity,
+                                uint32_t* overflow) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_request_scan<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024 * 8);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_request_scan<24>, cudaFuncAttributeMaxDynamicSharedMemorySize, 24 * 1024 * 8);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (R <= 4 * 1024)
+    k_request_scan<4><<<1, 1024, 4 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
+  else if (R <= 12 * 1024)
+    k_request_scan<12><<<1, 1024, 12 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
+  else
+    k_request_scan<24><<<1, 1024, 24 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
+  return cudaGetLastError();
 }
 
 // K3: stream compaction of the verdict bitmap into canonical-order indices.
@@ -1082,8 +1100,7 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   } else {
     AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
     Launch L(ctx, K_REQUEST_SCAN);
-    k_request_scan<<<1, 1024, 0, s>>>(out->counts, offsets, R,
-                                     out->indices ? out->capacity : ~0ULL, out->overflow);
+    AG_CUDA(launch_request_scan(s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
     AG_CUDA(cudaGetLastError());
     return AG_OK;
   }
@@ -1118,8 +1135,7 @@ int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin,
   }
   {
     Launch L(ctx, K_REQUEST_SCAN);
-    k_request_scan<<<1, 1024, 0, s>>>(out->counts, offsets, R,
-                                     out->indices ? out->capacity : ~0ULL, out->overflow);
+    AG_CUDA(launch_request_scan(s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
   }
   if (out->indices) {
     const int rc = launch_compact(ctx, R, W, C, begin, bitmap, offsets, out->indices, out->capacity);
