@@ -309,9 +309,18 @@ struct ScoreArgs {
 constexpr int kPatSeeds = 4;
 constexpr int kPatMax = 32;
 
-struct PatTable {
-  uint32_t lo[kPatSeeds][kPatMax];
-  uint32_t hi[kPatSeeds][kPatMax];
+union PatTable {
+  struct {
+    uint32_t lo[kPatSeeds][kPatMax];
+    uint32_t hi[kPatSeeds][kPatMax];
+  };
+  // up to two seeds (what the generator emits), rebuilt in place: the OR of
+  // the seeds' words for every subset of seeds whose prefix test passes,
+  // [phase][subset]
+  struct {
+    uint32_t clo[kPatMax][4];
+    uint32_t chi[kPatMax][4];
+  };
 };
 
 template <int NT>
@@ -385,8 +394,53 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
       }
     }
     __syncwarp();
+    if (k <= 2) {
+      PatTable& pt = s_pat[wid];
+      const bool own = lane < a.pat_P;
+      const uint32_t l0 = own && k > 0 ? pt.lo[0][lane] : 0u, l1 = own && k > 1 ? pt.lo[1][lane] : 0u;
+      const uint32_t h0 = own && k > 0 ? pt.hi[0][lane] : 0u, h1 = own && k > 1 ? pt.hi[1][lane] : 0u;
+      __syncwarp();  // the per-seed rows are read before the combinations overwrite them
+      pt.clo[lane][0] = 0u;
+      pt.clo[lane][1] = l0;
+      pt.clo[lane][2] = l1;
+      pt.clo[lane][3] = l0 | l1;
+      pt.chi[lane][0] = 0u;
+      pt.chi[lane][1] = h0;
+      pt.chi[lane][2] = h1;
+      pt.chi[lane][3] = h0 | h1;
+    }
+    __syncwarp();
   }
-  if (pat && full) {
+  if (pat && full && k <= 2) {
+    // hot path, at most two seeds: the prefix tests change only when the
+    // word crosses into the next block, so a word is two table loads
+    const WordPos p0 = word_pos(a.sp, i0s);
+    const uint32_t Bq = m * m;
+    uint32_t o = p0.x * m + p0.l0;
+    uint64_t Qn = q_add(p0.Q, 1, m, nq);
+    const int lg = a.pat_lg;
+    const PatTable& pt = s_pat[wid];
+    const uint64_t sq0 = k > 0 ? s_seeds[wid].q[0] : ~0ull, sq1 = k > 1 ? s_seeds[wid].q[1] : ~0ull;
+    auto tests = [&](uint64_t Q) -> uint32_t {  // bit s: every digit of Q >= seed s's
+      return (k > 0 && (((Q | a.H) - sq0) & a.H) == a.H ? 1u : 0u) |
+             (k > 1 && (((Q | a.H) - sq1) & a.H) == a.H ? 2u : 0u);
+    };
+    uint32_t mlo = tests(p0.Q), mhi = tests(Qn);
+#pragma unroll 4
+    for (uint32_t it = 0; it < 32; ++it) {
+      const uint32_t ph = o >> lg;
+      const uint32_t word = pt.clo[ph][mlo] | pt.chi[ph][mhi];
+      o += 32;
+      if (o >= Bq) {
+        o -= Bq;
+        Qn = q_add(Qn, 1, m, nq);
+        mlo = mhi;
+        mhi = tests(Qn);
+      }
+      cnt += __popc(word);
+      s_tr[wid][lane][it] = word;
+    }
+  } else if (pat && full) {
     // hot path: oracle router, no removals, 32 full words, phase tables
     const WordPos p0 = word_pos(a.sp, i0s);
     const uint32_t Bq = m * m;
