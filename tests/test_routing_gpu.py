@@ -98,6 +98,23 @@ def test_force_top_and_edge_sets():
             _check_against_oracle(dev, space, batch, router, force_top=ft)
 
 
+@pytest.mark.parametrize("n,m", [(5, 8), (4, 6), (6, 4)])
+def test_seed_counts_on_the_phase_pattern_path(n, m):
+    """Hand-built accurate sets with 0..6 seeds (the generator emits <= 2, the
+    ABI takes any seed CSR) on spaces where K1 takes its phase-pattern path
+    (M*M >= 32): the seed-subset tables (<= 2 seeds), the per-seed tests (3-4)
+    and the 2-D fallback (> 4), over full and ragged ranges."""
+    space = P.ConfigSpace.chain(n, m)
+    rng = np.random.default_rng(n * 100 + m)
+    seeds = []
+    for k in (0, 1, 2, 2, 3, 4, 5, 6, 1, 2):
+        seeds.append([[int(d) for d in rng.integers(0, m, n)] for _ in range(k)])
+    batch = P.AccuracyBatch.from_lists(n, seeds, [[] for _ in seeds])
+    dev = P.Device(space)
+    for a, b in ((0, space.size), (3, space.size - 5), (1024, min(space.size, 70000))):
+        _check_against_oracle(dev, space, batch, P.OracleRouter(), a, b)
+
+
 def test_subranges_concatenate_to_full_range():
     space = P.ConfigSpace.chain(5, 7)
     batch = P.AccuracyBatch.generate(space, P.GenParams(), 40, seed=9)
