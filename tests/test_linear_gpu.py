@@ -46,7 +46,10 @@ def _check(counts, offs, idx, bm, want, begin, end):
 
 
 @pytest.mark.parametrize("n,m,R,D,begin,end", [(5, 4, 300, 128, 0, None), (5, 6, 257, 64, 0, None),
-                                               (4, 6, 40, 128, 77, 1000), (3, 5, 513, 32, 5, 120)])
+                                               (4, 6, 40, 128, 77, 1000), (3, 5, 513, 32, 5, 120),
+                                               # D not a multiple of the 64-element TMA box: zero fill
+                                               (4, 5, 129, 16, 0, None), (4, 5, 200, 48, 1, 600),
+                                               (5, 5, 260, 80, 0, None), (4, 7, 70, 112, 100, 2401)])
 def test_integer_inputs_bit_exact(n, m, R, D, begin, end):
     sp = P.ConfigSpace.chain(n, m)
     end = sp.size if end is None else end
