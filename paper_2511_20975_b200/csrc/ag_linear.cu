@@ -40,7 +40,12 @@ namespace agb {
 namespace {
 
 #ifndef AG_LIN_EXP
-#define AG_LIN_EXP 0  // diagnostics: 1 = no threshold work, 2 = no TMEM loads either, 3 = spinning waits, 4 = B tiles loaded once (stale)
+// Diagnostic variants (scripts/linexp.sh; results are wrong by design except
+// 0 and 3): 1 = no threshold work, 2 = no TMEM loads either (the MMA pipeline
+// alone), 3 = spinning epilogue waits, 4 = B tiles loaded once (stale),
+// 5 = 2 with one request half's MMAs only, 6 = 2 with half the K steps,
+// 9 = 2 + 4, 10 = 2 without the TMEM-empty wait.
+#define AG_LIN_EXP 0
 #endif
 constexpr int kLinM = 128;        // requests per MMA (one TMEM lane each)
 constexpr int kLinR = 256;        // requests per work item (two MMAs per K step)
