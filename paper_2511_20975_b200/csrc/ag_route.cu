@@ -858,7 +858,10 @@ cudaError_t launch_request_scan(cudaStream_t s, const uint64_t* counts, uint64_t
 // full 16-byte vector is written back at once; the <= 3 trailing members carry
 // over to the next iteration, so global stores are almost all full vectors.
 constexpr int kStage = 32 * 32 + 8;  // one iteration's members + carry + pad
-constexpr uint32_t kUnitGroups = 8;
+#ifndef AG_UNIT_GROUPS
+#define AG_UNIT_GROUPS 4
+#endif
+constexpr uint32_t kUnitGroups = AG_UNIT_GROUPS;
 
 __global__ void __launch_bounds__(kThreads)
     k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ group_off,
