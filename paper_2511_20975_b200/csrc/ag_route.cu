@@ -40,7 +40,10 @@ namespace agb {
 
 namespace {
 
-constexpr int kWarpsPerBlock = 8;
+#ifndef AG_ROUTE_WARPS
+#define AG_ROUTE_WARPS 8
+#endif
+constexpr int kWarpsPerBlock = AG_ROUTE_WARPS;
 constexpr int kThreads = kWarpsPerBlock * 32;
 constexpr int kMaxFastSeeds = 32;    // per-warp packed-seed cache
 constexpr uint32_t kTaskIters = 32;  // iterations of 32 words per warp-task
