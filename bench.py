@@ -670,22 +670,73 @@ def run_ours(args):
         "path_roofline": {"bytes_per_step": path_bytes,
                           "achieved_gbs": path_bytes / (tot_ms / args.steps / 1e3) / 1e9,
                           "frac": path_bytes / (tot_ms / args.steps / 1e3) / 1e9 / hbm},
-        "kernel_share": kernel_share,
-        "members_per_step": total_members,
         "gpu_launches": int(launches),
-        "sched": sched,
-        "deep": deep,
-        "noisy": noisy,
-        "linear": linear,
-        "chain": chain,
-        "config5": config5,
         "clocks": clk,
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline()
+    # the legs' full records, then (last on the line, so the driver's
+    # 1,500-character stdout tail keeps it) the compact summary of every leg
+    line["detail"] = {"kernel_share": kernel_share, "members_per_step": total_members,
+                      "sched": sched, "deep": deep, "noisy": noisy, "linear": linear,
+                      "chain": chain, "config5": config5}
+    line["summary"] = summarize(line, sched, deep, noisy, linear, chain, config5)
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+def _r(x, nd=3):
+    return None if x is None else float(f"{x:.{nd}g}")
+
+
+def summarize(line, sched, deep, noisy, linear, chain, config5):
+    """One short record per leg (kept whole in the driver's stdout tail)."""
+    out = {"route_configs_per_s": _r(line["value"]), "route_e2e": _r(line["e2e"]["value"]),
+           "route_kernel_frac": _r(line["roofline"]["frac"])}
+    if sched:
+        out["sched_us"] = {"p50": _r(sched["p50_us"]), "p99": _r(sched["p99_us"]),
+                           "dev_p50": _r(sched["device_p50_us"]), "dev_p99": _r(sched["device_p99_us"]),
+                           "by_free": {k: [_r(v["p50_us"]), _r(v["p99_us"])]
+                                       for k, v in sched["by_free_slots"].items()},
+                           "hash": sched["decision_hash"]}
+        for name, v in (sched.get("variants") or {}).items():
+            out[f"sched_{name}_us"] = {"p50": _r(v["p50_us"]), "p99": _r(v["p99_us"]),
+                                       "by_free": {k: [_r(x["p50_us"]), _r(x["p99_us"])]
+                                                   for k, x in v["by_free_slots"].items()}}
+    if deep:
+        out["deep"] = {"configs_per_s": _r(deep["configs_per_s"]), "ms": _r(deep["ms_per_step"]),
+                       "n_gpus": deep["n_gpus"]}
+    if noisy:
+        out["noisy_configs_per_s"] = _r(noisy["configs_per_s"])
+    if linear:
+        out["linear"] = {"configs_per_s": _r(linear["configs_per_s"]),
+                         "tensor_frac": _r(linear["roofline"]["frac"])}
+    if chain:
+        out["chain_requests_per_s"] = _r(chain["requests_per_s"])
+    if config5:
+        out["config5"] = {"identical": config5["traces_identical"],
+                          "rounds_per_s": [[p["rate"], _r(p["gpu"]["rounds_per_s"]),
+                                            _r(p["reference"]["rounds_per_s"])]
+                                           for p in config5["points"]]}
+    return out
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without a launcher: re-exec under torchrun, one
+    process per GPU (rendezvous on 127.0.0.1)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -707,6 +758,7 @@ def main():
     ap.add_argument("--no-ubench", action="store_true",
                     help="skip the PCIe / absorb-rate microbenchmarks (e.g. under ncu)")
     args = ap.parse_args()
+    spawn_ranks(args)
     if args.impl == "reference":
         run_reference(args)
     else:

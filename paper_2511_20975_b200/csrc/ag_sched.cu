@@ -52,6 +52,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -61,6 +62,9 @@
 // Per-step phase timers of the walker (find / build / rank / adopt cycles,
 // ag_sched_round_timing slots 5-8): diagnostics, compiled in on request only
 // (-DAG_SCHED_PHASE_TIMERS=1) -- four clock reads per beam step otherwise.
+#ifndef AG_SCHED_WAITPROD
+#define AG_SCHED_WAITPROD 0
+#endif
 #ifndef AG_SCHED_PHASE_TIMERS
 #define AG_SCHED_PHASE_TIMERS 0
 #endif
@@ -81,8 +85,16 @@ namespace agb {
 
 namespace {
 
-constexpr int kRoundThreads = 512;
-constexpr int kProducers = 384;  // warps 1-3, 5-7, 9-11, 13-15
+// CTA shape of k_sched_round<BM>: warp 0 walks, the warps on its SM
+// sub-partition (wid % 4 == 0) stay idle, the others produce.  The fast
+// walker for B <= 4 keeps four beam states in every lane's registers, so its
+// CTA has 12 warps (168 registers per thread) instead of 16 (128).
+template <int BM>
+struct RoundShape {
+  static constexpr int threads = 512;
+  static constexpr int producers = threads / 4 * 3;  // warps 1-3, 5-7, 9-11 (, 13-15)
+};
+constexpr int kMaxRoundThreads = 512;
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
 constexpr int kSmemNodes = 1024;
@@ -107,6 +119,12 @@ struct Cand {  // one candidate pair
   uint32_t nvia;        // round-start viable size
 };
 
+// Engine pools in the kernel's internal order: weight descending, ties by
+// the caller's index (so the children of one state come out of a mask in
+// utilization order, fl(u + w) being monotone in w); inv[k] maps the caller's
+// engine k to its internal index for the order-sensitive folds
+// (initial_state and score_assignment sum over the caller's order) and the
+// occupancy output.
 struct EngDev {
   int E;
   int model[kMaxEng];
@@ -114,6 +132,7 @@ struct EngDev {
   int occ[kMaxEng];
   double weight[kMaxEng];
   int8_t m2e[32];  // model -> engine, -1 none
+  int8_t inv[kMaxEng];
   uint32_t mapped;  // models with a pool
 };
 
@@ -131,13 +150,11 @@ struct RoundArgs {
   const uint32_t* nviable;
   const uint64_t* ids;
   const uint32_t* ever;  // OR of every candidate-model mask ever installed
-  // round input deltas in mapped pinned host memory
-  const uint64_t* h_upd_mask;
-  const int32_t* h_upd_slot;
-  int n_upd;
-  const int32_t* h_tail;  // FIFO tail, lands at order[tail_from ..]
-  int tail_from, n_tail;
+  // round input deltas in mapped pinned host memory (or a DMA'd copy)
+  const int4* h_rec;      // refresh records {pos (-1: none), slot, ready lo, ready hi}
+  int n_rec;
   const int32_t* h_cidx;  // [Q] or null
+  uint4* pinfo;           // [Q] per-position pair records (see the setup)
   int8_t prio[64];
   int8_t prio_rank[64];
   uint32_t place[kMaxAgents];
@@ -155,12 +172,23 @@ struct RoundArgs {
   // outputs (mapped pinned host memory): [0] status [1] aux | ag_assignment |
   // occ[32] | triples
   int32_t* out;
+  uint32_t seq;  // round sequence number, written last (round_done)
   int triples_cap;
   unsigned long long* timing;  // [13]: globaltimer marks, walk/scan cycle buckets
   int32_t* async_status;       // errors latched by earlier dispatch / add kernels
 };
 
-constexpr int kOutHeader = 16;  // bytes before the ag_assignment
+constexpr int kOutHeader = 16;  // bytes before the ag_assignment: status, aux, round seq, pad
+
+// The round's last act: status (and aux) into the mapped result header, then
+// the round's sequence number, which the host spins on instead of a stream
+// synchronisation (the assignment is visible before the number).
+__device__ __forceinline__ void round_done(const RoundArgs& A, int status, int aux) {
+  A.out[1] = aux;
+  A.out[0] = status;
+  __threadfence_system();
+  *(volatile int32_t*)(A.out + 2) = (int32_t)A.seq;
+}
 
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
@@ -182,7 +210,8 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
                : "memory");
 }
 
-__device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory"); }
+template <int P>
+__device__ __forceinline__ void bar_producers() { asm volatile("bar.sync 1, %0;" ::"n"(P) : "memory"); }
 
 __device__ __forceinline__ uint32_t digit_at(uint32_t c, int a, const RoundArgs& A) {
   const uint32_t q = A.place[a] == 1 ? c : (uint32_t)__umul64hi(c, A.place_magic[a]);
@@ -256,6 +285,10 @@ __device__ __forceinline__ uint64_t rel_extend_sel(bool same, uint64_t r12, uint
   return same ? s_res : o_res;
 }
 
+// surv / initial for a histogram row the producers have not staged: out of
+// line, so the division is not if-converted into the walker's common path
+__device__ __noinline__ double ratio_slow(uint32_t surv, double initial) { return (double)surv / initial; }
+
 // order-preserving u64 image of an f64 (no NaNs here; -0 == +0)
 __device__ __forceinline__ uint64_t okey(double d) {
   uint64_t b = (uint64_t)__double_as_longlong(d);
@@ -280,12 +313,20 @@ struct Child {  // a BeamState child in shared memory (wide beams)
 };
 
 // ------------------------------------------------------------ round kernel
-__global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
+template <int BM>
+__global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(RoundArgs A) {
+  constexpr int kRoundThreads = RoundShape<BM>::threads, kProducers = RoundShape<BM>::producers;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int s_occ[2][kMaxBeam][kMaxEng];
   __shared__ uint64_t s_rel[2][kMaxBeam][kMaxBeam];
   __shared__ __align__(16) RankKey s_rk[32];
   __shared__ int s_cnt[kMaxBeam][32];
+  // fast walker: re-touch flex deltas, relevant-child keys, exact child order
+  __shared__ double s_rdelta[BM > 0 ? BM : 1][32];
+  __shared__ double2 s_fkey[32];
+  __shared__ unsigned long long s_fmeta[32];
+  __shared__ int8_t s_fe[32];
+  __shared__ int8_t s_order[BM > 0 ? BM : 1][8];
   __shared__ int s_picked[kMaxBeam];
   __shared__ int s_cons[kMaxAgents][2];
   __shared__ int s_ncons;
@@ -349,24 +390,17 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     }
     s_emtab[i >> 8][i & 255] = em;
   }
-  // the round's deltas (mapped host memory, small): FIFO tail, container
-  // indices, ready masks -- loads issued in batches so PCIe latency is paid
-  // once per batch
+  // The round's deltas (mapped host memory, small; one DMA copy when large):
+  // refresh records {FIFO position, slot, ready mask} for the rewritten FIFO
+  // range and for every other slot whose ready mask changed, and the
+  // container indices of a stateless call.  A record rewrites ready[slot],
+  // order[pos] and the position's pair record pinfo[pos] = {slot | first
+  // ready agent << 26, that agent's candidate-model mask, viable size,
+  // ready-agent count}, so the producers read one coalesced 16-byte record
+  // per FIFO position instead of the order -> ready -> cand gather chain.
+  // Loads are issued in batches so PCIe latency is paid once per batch.
   {
     constexpr int kU = 4;
-    for (int i0 = 0; i0 < A.n_tail; i0 += kRoundThreads * kU) {
-      int32_t v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kRoundThreads + tid;
-        v[u] = i < A.n_tail ? A.h_tail[i] : 0;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kRoundThreads + tid;
-        if (i < A.n_tail) A.order[A.tail_from + i] = v[u];
-      }
-    }
     if (A.h_cidx)
       for (int i0 = 0; i0 < A.Q; i0 += kRoundThreads * kU) {
         int32_t v[kU];
@@ -381,23 +415,44 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
           if (i < A.Q) A.cidx[i] = v[u];
         }
       }
-    for (int i0 = 0; i0 < A.n_upd; i0 += kRoundThreads * kU) {
-      int32_t sl[kU];
-      uint64_t mk[kU];
+    for (int i0 = 0; i0 < A.n_rec; i0 += kRoundThreads * kU) {
+      int4 rc[kU];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
         const int i = i0 + u * kRoundThreads + tid;
-        sl[u] = i < A.n_upd ? A.h_upd_slot[i] : -1;
-        mk[u] = i < A.n_upd ? A.h_upd_mask[i] : 0ull;
+        rc[u] = i < A.n_rec ? A.h_rec[i] : make_int4(-1, -1, 0, 0);
+      }
+      uint32_t cm[kU], nvv[kU];
+      int best[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int pos = rc[u].x, slot = rc[u].y;
+        const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
+        if (slot >= 0) A.ready[slot] = r;
+        // first ready agent in (depth desc, declaration asc) order
+        int bst = -1, br = 1 << 30;
+        for (uint64_t b = r; b; b &= b - 1) {
+          const int ag = __ffsll((long long)b) - 1;
+          if (A.prio_rank[ag] < br) br = A.prio_rank[ag], bst = ag;
+        }
+        best[u] = bst;
+        cm[u] = pos >= 0 && bst >= 0 ? A.cand[(size_t)slot * N + bst] : 0u;
+        nvv[u] = pos >= 0 ? A.nviable[slot] : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < kU; ++u)
-        if (sl[u] >= 0) A.ready[sl[u]] = mk[u];
+      for (int u = 0; u < kU; ++u) {
+        const int pos = rc[u].x, slot = rc[u].y;
+        if (pos < 0) continue;
+        const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
+        A.order[pos] = slot;
+        A.pinfo[pos] = make_uint4((uint32_t)slot | ((uint32_t)(best[u] & 63) << 26), cm[u], nvv[u],
+                                  (uint32_t)__popcll(r));
+      }
     }
   }
   __syncthreads();
   if (s_status) {
-    if (tid == 0) A.out[0] = s_status;
+    if (tid == 0) round_done(A, s_status, 0);
     return;
   }
   if (tid == 0 && A.timing) A.timing[1] = gtimer();
@@ -417,6 +472,13 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     // ================================================= producers
     const int pt = tid - 32 * (1 + (wid >> 2));  // 0 .. kProducers-1
     const int pw = pt >> 5;
+    // the next chunk's pair records are loaded while this one is processed
+    uint4 inf[kPer], nxt[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      const int p = pt * kPer + i;
+      nxt[i] = p < A.Q ? A.pinfo[p] : make_uint4(0u, 0u, 0u, 0u);
+    }
     for (int base = 0; base < A.Q; base += kProducers * kPer) {
       if (s_stop) break;  // uniform: written before the previous barrier
       const int p0 = base + pt * kPer;
@@ -424,23 +486,22 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       uint64_t rdy[kPer];
       uint32_t cm1[kPer], nvia[kPer];
 #pragma unroll
-      for (int i = 0; i < kPer; ++i) slot[i] = p0 + i < A.Q ? A.order[p0 + i] : -1;
-#pragma unroll
-      for (int i = 0; i < kPer; ++i) rdy[i] = slot[i] >= 0 ? A.ready[slot[i]] : 0ull;
+      for (int i = 0; i < kPer; ++i) {
+        inf[i] = nxt[i];
+        const int p = p0 + kProducers * kPer + i;
+        nxt[i] = p < A.Q ? A.pinfo[p] : make_uint4(0u, 0u, 0u, 0u);
+      }
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
-        // first ready agent in (depth desc, declaration asc) order
-        int best = -1, br = 1 << 30;
-        for (uint64_t b = rdy[i]; b; b &= b - 1) {
-          const int a = __ffsll((long long)b) - 1;
-          if (s_prank[a] < br) br = s_prank[a], best = a;
-        }
-        a1[i] = best;
-        cm1[i] = best >= 0 ? A.cand[(size_t)slot[i] * N + best] : 0u;
-        nvia[i] = best >= 0 ? A.nviable[slot[i]] : 0u;
+        slot[i] = (int)(inf[i].x & 0x3ffffffu);
+        a1[i] = (int)(inf[i].x >> 26);
+        cm1[i] = inf[i].y;
+        nvia[i] = inf[i].z;
+        // the full ready mask only for requests with parallel ready agents
+        rdy[i] = inf[i].w > 1u ? A.ready[slot[i]] : (inf[i].w ? 1ull << a1[i] : 0ull);
       }
       // pass 1: counts (pairs, requests, candidates) of this thread's positions
-      long long np = 0, nq = 0, nc = 0;
+      int np = 0, nq = 0, nc = 0;
       bool bad = false;
 #pragma unroll
       for (int i = 0; i < kPer; ++i) {
@@ -461,42 +522,42 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       }
       if (bad) s_status = AG_ERR_VALIDATION + 100;  // viable tier without a pool
       if (base == 0 && pt == 0 && A.timing) A.timing[11] = gtimer();
-      long long x[3] = {np, nq, nc};
+      int x[3] = {np, nq, nc};
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const long long y = __shfl_up_sync(kFull, x[k], o);
+          const int y = __shfl_up_sync(kFull, x[k], o);
           if (lane >= o) x[k] += y;
         }
       if (lane == 31)
 #pragma unroll
         for (int k = 0; k < 3; ++k) s_scan[pw][k] = x[k];
-      bar_producers();
+      bar_producers<kProducers>();
       if (pw == 0) {
         constexpr int NW = kProducers / 32;
-        long long v[3], z[3];
+        int v[3], z[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) v[k] = z[k] = lane < NW ? s_scan[lane][k] : 0;
+        for (int k = 0; k < 3; ++k) v[k] = z[k] = lane < NW ? (int)s_scan[lane][k] : 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1)
+        for (int o = 1; o < NW; o <<= 1)
 #pragma unroll
           for (int k = 0; k < 3; ++k) {
-            const long long y = __shfl_up_sync(kFull, z[k], o);
+            const int y = __shfl_up_sync(kFull, z[k], o);
             if (lane >= o) z[k] += y;
           }
         if (lane < NW)
 #pragma unroll
           for (int k = 0; k < 3; ++k) s_scan[lane][k] = z[k] - v[k] + s_carry[k];
         __syncwarp();
-        if (lane == 31) {
+        if (lane == NW - 1) {
           s_chunk[0] = (int)s_carry[2];
 #pragma unroll
           for (int k = 0; k < 3; ++k) s_carry[k] += z[k];
           s_chunk[1] = (int)s_carry[2];
         }
       }
-      bar_producers();
+      bar_producers<kProducers>();
       if (base == 0 && pt == 0 && A.timing) A.timing[12] = gtimer();
       // pass 2: this thread's candidates (position, engine mask, details) in pair order
       int pos = (int)(s_scan[pw][0] + x[0] - np);
@@ -531,7 +592,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
           if (single) break;
         }
       }
-      bar_producers();
+      bar_producers<kProducers>();
       if (base == 0 && pt == 0 && A.timing) A.timing[13] = gtimer();
       // pass 3: for the head of the list, the histogram rows with the
       // first-touch flexibility ratios (extend_state, scheduler.cpp:182-191)
@@ -568,7 +629,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
         }
       };
       stage_rows(c_lo, c_mid);
-      bar_producers();
+      bar_producers<kProducers>();
       if (pt == 0) {
         if (base == 0 && A.timing) A.timing[14] = gtimer();
         __threadfence_block();
@@ -577,14 +638,14 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
       }
       if (c_hi > c_mid) {
         stage_rows(c_mid, c_hi);
-        bar_producers();
+        bar_producers<kProducers>();
         if (pt == 0) {
           __threadfence_block();
           st_release(&s_rows, (unsigned)c_hi);
         }
       }
       if (pt == 0) s_stop = check_all ? 0 : (int)*(volatile unsigned*)&s_walk_done;
-      bar_producers();
+      bar_producers<kProducers>();
     }
     if (pt == 0) {
       if (A.timing) A.timing[15] = gtimer();  // producers done
@@ -607,7 +668,8 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   long long st_sk = 0;
   uint32_t st_fm = 0;
   if (lane == 0) {
-    for (int e = 0; e < E; ++e) {
+    for (int k = 0; k < E; ++k) {  // the caller's engine order (utilization fold)
+      const int e = A.eng.inv[k];
       const int occ = A.eng.occ[e];
       if (occ > e_slots[e]) wstatus = AG_ERR_VALIDATION + 200;  // engine over capacity
       s_occ[0][0][e] = occ;
@@ -619,7 +681,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   __syncwarp();
   // occupancy of state w, engine e in lane (w << lgE) + e when every state's
   // row fits the warp (B * E padded <= 32); shared-memory rows otherwise
-  const bool regocc = (B << lgE) <= 32;
+  const bool regocc = BM == 0 && (B << lgE) <= 32;
   const int ow = lane >> lgE, oe = lane & ((1 << lgE) - 1);
   int occ_r = (ow == 0 && oe < E) ? A.eng.occ[oe] : 0;
   int cur = 0, nst = 1, nnodes = 0;
@@ -654,6 +716,14 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   auto maskf = [&](int i) -> uint32_t { return i < A.cand_cap ? c_mask[i] : A.gmask[i - A.cand_cap]; };
   auto recf = [&](int i) -> Cand { return i < A.cand_cap ? c_rec[i] : A.grec[i - A.cand_cap]; };
 
+  if constexpr (BM > 0) {
+#if AG_SCHED_WAITPROD  // diagnostics: walk only after the producers are done
+    if (lane == 0)
+      while (!ld_acquire(&s_prod_done)) __nanosleep(64);
+    __syncwarp();
+#endif
+#include "ag_sched_fast.cuh"
+  } else
   while (!wstatus) {
     const uint32_t U = __reduce_or_sync(kFull, lane < nst ? st_fm : 0u);
     if (!U) break;  // all-full early exit (scheduler.cpp:303-315)
@@ -1073,7 +1143,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
     if (s_status) wstatus = s_status;
   }
   if (wstatus) {
-    if (lane == 0) A.out[0] = wstatus;
+    if (lane == 0) round_done(A, wstatus, 0);
     return;
   }
   {  // the remaining pairs are skips (all-full exit or no candidate left)
@@ -1110,10 +1180,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   int32_t* occ_out = reinterpret_cast<int32_t*>(res + 1);
   ag_triple* triples = reinterpret_cast<ag_triple*>(occ_out + kMaxEng);
   if (D > A.triples_cap) {
-    if (lane == 0) {
-      A.out[0] = AG_ERR_VALIDATION + 400;
-      A.out[1] = D;
-    }
+    if (lane == 0) round_done(A, AG_ERR_VALIDATION + 400, D);
     return;
   }
   // the path, root first (node ids into the children area, free now)
@@ -1194,14 +1261,15 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   if (lane != 0) return;
   // score_assignment: utilization in engine order
   double util = 0.0;
-  for (int e = 0; e < E; ++e) {
+  for (int k = 0; k < E; ++k) {  // the caller's engine order
+    const int e = A.eng.inv[k];
     const int o = s_occ[cur][best][e];
     if (o < 0 || o > e_slots[e]) {
-      A.out[0] = AG_ERR_VALIDATION + 500;
+      round_done(A, AG_ERR_VALIDATION + 500, 0);
       return;
     }
     util += o * e_weight[e];
-    occ_out[e] = o;
+    occ_out[k] = o;
   }
   ag_assignment r;
   r.n_triples = D;
@@ -1212,8 +1280,7 @@ __global__ void __launch_bounds__(kRoundThreads, 1) k_sched_round(RoundArgs A) {
   r.states_explored = explored;
   *res = r;
   if (A.timing) A.timing[4] = gtimer();
-  A.out[1] = 0;
-  A.out[0] = 0;
+  round_done(A, 0, 0);
 }
 
 // ------------------------------------------------------------ prune kernel
@@ -1371,6 +1438,8 @@ struct ag_sched {
   // device queue order: live and dead (ready 0) slots in FIFO order; host copy
   std::vector<int32_t> order;
   size_t dirty_from = 0;  // device copy valid before this index
+  size_t pinfo_from = 0;  // device pair records (pinfo) valid before this index
+  std::vector<int32_t> pos_of;  // slot -> FIFO position (-1: not listed)
   size_t dead = 0;
   std::vector<int32_t> upd_slot;
   std::vector<uint64_t> upd_mask;
@@ -1381,9 +1450,11 @@ struct ag_sched {
   uint32_t place[agb::kMaxAgents];
   uint64_t place_magic[agb::kMaxAgents];
   bool attr_set = false;
+  int walker = 0;  // AG_SCHED_WALKER: 0 automatic, 1 always the general walker
+  uint32_t round_seq = 0;
   double last_round_us = 0.0;
   // device
-  agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx;
+  agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx, d_pinfo;
   agb::Scratch d_cpos, d_det, d_nodes, d_status, d_gam, d_qa, d_upd;  // d_cpos / d_det: candidate overflow
   // pinned host staging
   void* h_res = nullptr;
@@ -1456,10 +1527,14 @@ bool fifo_less(const ag_sched* s, int x, int y) {
 void compact_order(ag_sched* s) {
   std::vector<int32_t> live_order;
   live_order.reserve(s->order.size());
-  for (int slot : s->order)
+  for (int slot : s->order) {
+    s->pos_of[slot] = -1;
     if (s->live[slot]) live_order.push_back(slot);
+  }
   s->order.swap(live_order);
+  for (size_t p = 0; p < s->order.size(); ++p) s->pos_of[s->order[p]] = (int32_t)p;
   s->dirty_from = 0;
+  s->pinfo_from = 0;
   s->dead = 0;
   s->free_slots.insert(s->free_slots.end(), s->quarantine.begin(), s->quarantine.end());
   s->quarantine.clear();
@@ -1529,27 +1604,39 @@ int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vec
   return AG_OK;
 }
 
-int engines_dev(const ag_engines* e, EngDev* out) {
+int engines_dev(const ag_engines* e, EngDev* out, bool* ordered = nullptr) {
   // RoundContext validation (scheduler.cpp:39-52)
   if (!e) return fail(AG_ERR_VALIDATION, "engines is null");
   if (e->n_engines > kMaxEng) return fail(AG_ERR_VALIDATION, "more engine pools than the scheduler supports");
   EngDev d{};
   d.E = e->n_engines;
   for (int i = 0; i < 32; ++i) d.m2e[i] = -1;
+  bool nan = false;
   for (int i = 0; i < d.E; ++i) {
     const int mdl = e->model[i];
     if (mdl < 0) return fail(AG_ERR_VALIDATION, "engine with negative model tier");
     for (int k = 0; k < i; ++k)
       if (e->model[k] == mdl) return fail(AG_ERR_VALIDATION, "two engine pools serve the same model tier");
+    nan |= std::isnan(e->weight[i]);
+  }
+  // internal order: weight descending, ties by the caller's index
+  std::vector<int> ord(d.E);
+  std::iota(ord.begin(), ord.end(), 0);
+  if (!nan) std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return e->weight[x] > e->weight[y]; });
+  for (int i = 0; i < d.E; ++i) {
+    const int k = ord[i];
+    const int mdl = e->model[k];
     if (mdl < 32) {
       d.m2e[mdl] = (int8_t)i;
       d.mapped |= 1u << mdl;
     }
     d.model[i] = mdl;
-    d.slots[i] = e->slots[i];
-    d.occ[i] = e->occupancy[i];
-    d.weight[i] = e->weight[i];
+    d.slots[i] = e->slots[k];
+    d.occ[i] = e->occupancy[k];
+    d.weight[i] = e->weight[k];
+    d.inv[k] = (int8_t)i;
   }
+  if (ordered) *ordered = !nan;
   *out = d;
   return AG_OK;
 }
@@ -1564,8 +1651,13 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   if (B < 1) return fail(AG_ERR_VALIDATION, "beam width < 1");
   if (B > kMaxBeam) return fail(AG_ERR_VALIDATION, "GPU scheduler supports beam width <= 32");
   EngDev ed;
-  int rc = engines_dev(engines, &ed);
+  bool ordered = false;
+  int rc = engines_dev(engines, &ed, &ordered);
   if (rc) return rc;
+  // the fast walker (ag_sched_fast.cuh): B <= 4, <= 8 pools of <= 255 free slots
+  bool fast = ordered && B <= 4 && ed.E <= 8;
+  for (int i = 0; i < ed.E; ++i) fast &= ed.slots[i] - ed.occ[i] <= 255;
+  const int bm = fast && s->walker != 1 ? (B == 1 ? 1 : 4) : 0;
   int total_free = 0;
   for (int i = 0; i < ed.E; ++i) total_free += std::max(0, ed.slots[i] - ed.occ[i]);
   const int Q = (int)s->order.size();
@@ -1590,12 +1682,15 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
     s->upd_mask.erase(s->upd_mask.begin(), s->upd_mask.begin() + w);
   }
   const size_t nu = s->upd_slot.size();
-  const size_t tail_from = std::min<size_t>(s->dirty_from, (size_t)Q);
-  const size_t n_tail = Q - tail_from;
-  // mapped staging: masks | slots | FIFO tail | container indices
-  const size_t off_slot = nu * 8;
-  const size_t off_tail = off_slot + nu * 4;
-  const size_t off_cidx = off_tail + n_tail * 4;
+  // refresh records: every FIFO position from the first stale one, then the
+  // other slots whose ready mask changed (the host mirror holds the masks)
+  const size_t from = std::min(std::min(s->dirty_from, s->pinfo_from), (size_t)Q);
+  size_t n_rec = (size_t)Q - from;
+  for (size_t i = 0; i < nu; ++i) {
+    const int32_t p = s->pos_of[s->upd_slot[i]];
+    n_rec += !(p >= 0 && (size_t)p >= from);
+  }
+  const size_t off_cidx = n_rec * 16;
   const size_t up_bytes = off_cidx + (cidx_host ? (size_t)Q * 4 : 0) + 16;
   const size_t res_bytes = kOutHeader + sizeof(ag_assignment) + 4 * kMaxEng + (size_t)cap_t * sizeof(ag_triple);
   if ((rc = ensure_pinned(&s->h_rstage, &s->h_rstage_bytes, up_bytes)) ||
@@ -1604,9 +1699,19 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
     return rc;
   // the previous round synchronised after its last use of h_rstage / h_res
   char* h = (char*)s->h_rstage;
-  std::memcpy(h, s->upd_mask.data(), nu * 8);
-  std::memcpy(h + off_slot, s->upd_slot.data(), nu * 4);
-  std::memcpy(h + off_tail, s->order.data() + tail_from, n_tail * 4);
+  {
+    int32_t* r = reinterpret_cast<int32_t*>(h);
+    auto put = [&](int32_t pos, int32_t slot) {
+      const uint64_t m = s->ready[slot];
+      r[0] = pos, r[1] = slot, r[2] = (int32_t)(uint32_t)m, r[3] = (int32_t)(uint32_t)(m >> 32);
+      r += 4;
+    };
+    for (size_t p = from; p < (size_t)Q; ++p) put((int32_t)p, s->order[p]);
+    for (size_t i = 0; i < nu; ++i) {
+      const int32_t p = s->pos_of[s->upd_slot[i]];
+      if (!(p >= 0 && (size_t)p >= from)) put(p, s->upd_slot[i]);
+    }
+  }
   if (cidx_host) std::memcpy(h + off_cidx, cidx_host, (size_t)Q * 4);
   if (s->h_rstage != s->h_rstage_mapped) {
     if ((rc = dev_ptr(s->h_rstage, &s->h_rstage_dev))) return rc;
@@ -1649,7 +1754,9 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
       (rc = s->d_nodes.ensure((size_t)std::max(1, max_nodes - kSmemNodes) * sizeof(Node))))
     return rc;
   if (!s->attr_set) {
-    AG_CUDA(cudaFuncSetAttribute(k_sched_round, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn));
+    AG_CUDA(cudaFuncSetAttribute(k_sched_round<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn));
+    AG_CUDA(cudaFuncSetAttribute(k_sched_round<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn));
+    AG_CUDA(cudaFuncSetAttribute(k_sched_round<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)max_dyn));
     s->attr_set = true;
   }
   RoundArgs A;
@@ -1669,13 +1776,10 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.nviable = (const uint32_t*)s->d_nv.p;
   A.ids = (const uint64_t*)s->d_ids.p;
   A.ever = (const uint32_t*)((char*)s->d_status.p + 8);
-  A.h_upd_mask = (const uint64_t*)hd;
-  A.h_upd_slot = (const int32_t*)(hd + off_slot);
-  A.n_upd = (int)nu;
-  A.h_tail = (const int32_t*)(hd + off_tail);
-  A.tail_from = (int)tail_from;
-  A.n_tail = (int)n_tail;
+  A.h_rec = (const int4*)hd;
+  A.n_rec = (int)n_rec;
   A.h_cidx = cidx_host ? (const int32_t*)(hd + off_cidx) : nullptr;
+  A.pinfo = (uint4*)s->d_pinfo.p;
   std::memcpy(A.prio, s->prio, sizeof A.prio);
   for (int t = 0; t < s->N; ++t) A.prio_rank[(int)s->prio[t]] = (int8_t)t;
   std::memcpy(A.place, s->place, sizeof A.place);
@@ -1691,16 +1795,28 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.max_nodes = max_nodes;
   A.max_children = max_children;
   A.out = out_d;
+  A.seq = ++s->round_seq;
   A.triples_cap = cap_t;
   A.timing = (unsigned long long*)((char*)s->d_status.p + 32);
   A.async_status = (int32_t*)s->d_status.p;
   {
     Launch L(ctx, K_SCHED_ROUND);
-    k_sched_round<<<1, kRoundThreads, dyn, ctx->stream>>>(A);
+    if (bm == 1) k_sched_round<1><<<1, RoundShape<1>::threads, dyn, ctx->stream>>>(A);
+    else if (bm == 4) k_sched_round<4><<<1, RoundShape<4>::threads, dyn, ctx->stream>>>(A);
+    else k_sched_round<0><<<1, RoundShape<0>::threads, dyn, ctx->stream>>>(A);
   }
   AG_CUDA(cudaGetLastError());
-  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  {
+    // spin on the round's sequence number in the mapped result header (a
+    // stream synchronisation costs several microseconds more); a kernel that
+    // ends without writing it (a fault) is caught by the stream query
+    volatile const int32_t* flag = (volatile const int32_t*)s->h_res + 2;
+    for (unsigned it = 1; *flag != (int32_t)A.seq; ++it)
+      if ((it & 1023u) == 0 && cudaStreamQuery(ctx->stream) != cudaErrorNotReady) break;
+    if (*flag != (int32_t)A.seq) AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   s->dirty_from = Q;
+  s->pinfo_from = Q;
   s->upd_slot.clear();
   s->upd_mask.clear();
   const char* hr = (const char*)s->h_res;
@@ -1730,8 +1846,10 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
 // Empties a session for reuse (stateless beam_schedule): host mirror back to
 // its initial state; device arrays are rewritten by the next add before use.
 void reset_session(ag_sched* s) {
+  for (int slot : s->order) s->pos_of[slot] = -1;
   s->order.clear();
   s->dirty_from = 0;
+  s->pinfo_from = 0;
   s->dead = 0;
   s->quarantine.clear();
   s->free_slots.clear();
@@ -1777,11 +1895,13 @@ int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_
   s->M = sp->m;
   s->cap = max_requests;
   s->pool_cap = std::max<uint64_t>(max_configs, 1);
+  if (const char* w = std::getenv("AG_SCHED_WALKER")) s->walker = std::strcmp(w, "general") == 0 ? 1 : 0;
   s->ids.assign(max_requests, 0);
   s->arrival.assign(max_requests, 0.0);
   s->stages.assign((size_t)max_requests * sp->n, 0);
   s->ready.assign(max_requests, 0);
   s->live.assign(max_requests, 0);
+  s->pos_of.assign(max_requests, -1);
   s->nviable.assign(max_requests, 0);
   for (int i = max_requests - 1; i >= 0; --i) s->free_slots.push_back(i);
   // agent priority: depth descending, declaration ascending (scheduler.cpp:238-242)
@@ -1804,7 +1924,8 @@ int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_
       (rc = s->d_hist.ensure(R * sp->n * sp->m * 4)) || (rc = s->d_nv.ensure(R * 4)) ||
       (rc = s->d_voff.ensure(R * 8)) || (rc = s->d_ids.ensure(R * 8)) ||
       (rc = s->d_pool.ensure(s->pool_cap * 4)) || (rc = s->d_status.ensure(192)) ||
-      (rc = s->d_order.ensure(((size_t)2 * max_requests + 1024) * 4))) {
+      (rc = s->d_order.ensure(((size_t)2 * max_requests + 1024) * 4)) ||
+      (rc = s->d_pinfo.ensure(((size_t)2 * max_requests + 1024) * 16))) {
     delete s;
     return rc;
   }
@@ -1878,7 +1999,9 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
                      s->order.begin());
     }
     s->order.insert(s->order.begin() + pos, slot);
+    for (size_t k = pos; k < s->order.size(); ++k) s->pos_of[s->order[k]] = (int32_t)k;
     s->dirty_from = std::min(s->dirty_from, pos);
+    s->pinfo_from = std::min(s->pinfo_from, pos);
   }
   // the viable copy must land before the histogram pass reads it (same stream)
   const int rc = agb::launch_prune(s, slots, g_begin, {}, &meta);

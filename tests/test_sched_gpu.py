@@ -198,3 +198,55 @@ def test_session_multi_round_matches_oracle(shape, nreq, width, seed):
         inflight = keep
         for s in list(by_slot)[:50]:
             assert sess.viable(s).tolist() == by_slot[s]["viable"]
+
+
+def _tie_case(rng, n, m, edges, nreq, weights, slots_cap):
+    sp = P.ConfigSpace(n, edges, [1.0 + i for i in range(m)], [8.0 / 1.5 ** i for i in range(m)])
+    pred_mask = [sum(1 << a for a, b in edges if b == x) for x in range(n)]
+    reqs = []
+    for r in range(nreq):
+        stages = [1 if pred_mask[a] == 0 else 0 for a in range(n)]
+        k = int(rng.integers(1, min(sp.size, 12) + 1))
+        viable = sorted(set(int(x) for x in rng.integers(0, sp.size, size=k)))
+        reqs.append(dict(id=int(500 + r), arrival=float(rng.integers(0, 5)), stages=stages, viable=viable))
+    occ = [int(rng.integers(0, c + 1)) for c in slots_cap]
+    eng = P.Engines(list(range(m)), slots_cap, occ, weights)
+    return sp, reqs, eng
+
+
+@pytest.mark.parametrize("walker", ["auto", "general"])
+def test_beam_ties_match_oracle(walker, monkeypatch):
+    """Equal and near-equal engine weights (utilization ties inside one
+    parent's children and across parents, decided by flexibility, skips and
+    triples_less), widths 1-4 (the fast walker) and 6 (the general one),
+    chains and diamonds, against the C oracle."""
+    if walker == "general":
+        monkeypatch.setenv("AG_SCHED_WALKER", "general")
+    rng = np.random.default_rng(11)
+    weight_sets = [[1.0, 1.0, 1.0], [2.0, 1.0, 1.0, 0.5], [0.1, 0.2, 0.3, 0.3, 0.1],
+                   [1.0, 1.0 + 2 ** -52, 1.0, 0.5], [3.0, 3.0, 3.0, 3.0, 3.0, 3.0, 3.0, 3.0]]
+    devs = {}
+    for case in range(60):
+        ws = weight_sets[case % len(weight_sets)]
+        m = len(ws)
+        if case % 3 == 2:
+            n, edges = 4, DIAMOND
+        else:
+            n, edges = 3, [(0, 1), (1, 2)]
+        cap = [int(rng.integers(1, 4)) for _ in range(m)]
+        sp, reqs, eng = _tie_case(rng, n, m, edges, int(rng.integers(3, 25)), ws, cap)
+        key = (n, m, len(edges))
+        if key not in devs:
+            devs[key] = P.Device(sp)
+        dev = devs[key]
+        q = P.Queue(n, [r["id"] for r in reqs], [r["arrival"] for r in reqs],
+                    [s for r in reqs for s in r["stages"]], [r["viable"] for r in reqs])
+        order = sorted(range(len(reqs)), key=lambda i: (reqs[i]["arrival"], reqs[i]["id"]))
+        for width in (1, 2, 3, 4, 6):
+            want = _oracle_round(n, m, sp.depth.tolist(), sp.decl.tolist(), reqs, eng, width)
+            got = P.beam_schedule(dev, q, eng, width)
+            assert [list(t) for t in got.triples] == [list(t) for t in want["triples"]], (case, width)
+            assert got.occupancy == want["occupancy"], (case, width)
+            assert got.utilization == want["utilization"] and got.flexibility == want["flexibility"]
+            assert got.skips == want["skips"] and got.states_explored == want["states_explored"]
+        del order
