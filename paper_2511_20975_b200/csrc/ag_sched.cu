@@ -1795,7 +1795,11 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.max_nodes = max_nodes;
   A.max_children = max_children;
   A.out = out_d;
-  A.seq = ++s->round_seq;
+  // the host spins on this number in the mapped header: clear the word first
+  // (a fresh or recycled pinned buffer may hold any value) and never use 0
+  if (++s->round_seq == 0) s->round_seq = 1;
+  A.seq = s->round_seq;
+  ((volatile int32_t*)s->h_res)[2] = 0;
   A.triples_cap = cap_t;
   A.timing = (unsigned long long*)((char*)s->d_status.p + 32);
   A.async_status = (int32_t*)s->d_status.p;
