@@ -147,6 +147,38 @@ def ref_sched(rounds, beam=SCHED_BEAM, exhaustive=False):
     return json.loads(out.strip().splitlines()[-1])
 
 
+SELECT_CPU_SAMPLE = {"exhaustive": 1000, "viable": REQUESTS_PER_GPU}
+
+
+def ref_select(sets, requests, threads):
+    out = subprocess.run([REF_BENCH, "select", str(N_AGENTS), str(N_TIERS), str(requests), str(threads),
+                          str(SEED), sets], capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def select_load(m):
+    """The select leg's load context (ref_bench select): occupancy 4,
+    queued_ahead i % 3, 8 slots, ServiceTimeModel{mu -0.3 + 0.35 i, sigma
+    0.25, floor 0.05}::mean computed with the C library's exp, as the
+    reference does (engine.cpp:62-65)."""
+    import math
+
+    mean = [0.05 + math.exp((-0.3 + 0.35 * i) + 0.5 * 0.25 * 0.25) for i in range(m)]
+    return [4] * m, [i % 3 for i in range(m)], [8] * m, mean
+
+
+def select_digest(chosen, est, n):
+    """ref_bench select's digest: D = mix({D, index, estimate bits}) over
+    the first n requests."""
+    from paper_2511_20975_b200 import workloads as W
+
+    bits = np.asarray(est[:n], np.float64).view(np.uint64)
+    d = 0x5EED
+    for i in range(n):
+        d = W.mix(d, int(chosen[i]), int(bits[i]))
+    return f"{d:016x}"
+
+
 # config-3 variants beside the headline (B = 4, predictor sets): the other
 # beam width SURVEY.md §8(d) names, and exhaustive viable sets (the full
 # accurate set per request, 13.5k configurations on average)
@@ -255,6 +287,13 @@ def run_reference(args):
             r = ref_sched(sv["ref_rounds"], sv["beam"], sv["exhaustive"])
             variants[name] = {"beam": sv["beam"], "exhaustive": sv["exhaustive"],
                               "p50_us": r["p50_us"], "p99_us": r["p99_us"], "rounds": r["rounds"]}
+    select = {}
+    if not args.no_select:
+        for sets in ("exhaustive", "viable"):
+            r = ref_select(sets, SELECT_CPU_SAMPLE[sets], threads)
+            select[sets] = {"configs_costed_per_s": r["configs_costed_per_s"],
+                            "us_per_batch": r["us_per_request"] * REQUESTS_PER_GPU,
+                            "sample": f"first {SELECT_CPU_SAMPLE[sets]} requests", "cores": threads}
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
@@ -265,7 +304,8 @@ def run_reference(args):
             "sched": {"p50_us": sched["p50_us"], "p99_us": sched["p99_us"],
                       "mean_us": sched["mean_us"], "rounds": sched["rounds"], "cores": 1,
                       "decision_hash": sched["hash"], "variants": variants,
-                      "what": "beam_schedule per round, reference C++ on one core"}}
+                      "what": "beam_schedule per round, reference C++ on one core"},
+            "select": select}
     print(json.dumps(line))
 
 
@@ -302,6 +342,58 @@ def run_sched(P, W, dev, args, rounds=None, beam=SCHED_BEAM, exhaustive=False):
             "decision_hash": f"{h:016x}",
             "what": "ag_sched_round wall time inside the C ABI (update upload + round kernel + "
                     "assignment download); device = the round kernel alone"}
+
+
+def run_select(P, dev, sets, members, offsets, n_members, stream, flush, barrier, with_ref):
+    """The per-stage re-cost + argmin of config 3:
+    select_per_input_config(set, space, kPerInputRuntimeCost, &ctx) for all
+    10k requests of the batch, device-resident member CSR, CUDA-event timed
+    (µs per 10k-request batch), HBM roofline at 4 B read per member; the
+    reference (ref_bench select) on all host cores beside it, and the digest
+    of (chosen, estimate) over its sample equal to the reference's."""
+    import torch
+
+    m = dev.space.m
+    occ, queued, slots, mean = select_load(m)
+    load = P.RuntimeCostContext(occ, queued, slots, mean)
+    R = REQUESTS_PER_GPU
+    for _ in range(3):
+        ch, est = P.select_per_input(dev, members, offsets, P.PER_INPUT_RUNTIME_COST, load,
+                                     check_errors=False)
+    dev.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    barrier()
+    dev.profile_begin()
+    for i in range(10):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(stream)
+        ch, est = P.select_per_input(dev, members, offsets, P.PER_INPUT_RUNTIME_COST, load,
+                                     check_errors=False)
+        ev[i][1].record(stream)
+    kprof = dev.profile_end()
+    dev.synchronize()
+    ms = statistics.median([a.elapsed_time(b) for a, b in ev])
+    kms = kprof["k_cost_argmin"][0] / 10 if "k_cost_argmin" in kprof else ms
+    hbm, psrc = peaks()
+    out = {"workload": f"config3 re-cost + argmin: select_per_input_config(kPerInputRuntimeCost) over "
+                       f"the {sets} sets of {R} config-2 requests ({n_members} members), load context "
+                       "of ref_bench select",
+           "us_per_batch": ms * 1e3, "configs_costed_per_s": n_members / (ms / 1e3),
+           "launches_per_batch": 4,
+           "roofline": {"bound": "hbm", "kernel": "k_cost_plan/prefix/tasks/reduce",
+                        "achieved": 4.0 * n_members / (kms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                        "frac": 4.0 * n_members / (kms / 1e3) / 1e9 / hbm, "peak_source": psrc,
+                        "algorithmic_bytes_per_launch": 4 * n_members}}
+    if with_ref and os.path.exists(REF_BENCH):
+        n = SELECT_CPU_SAMPLE[sets]
+        ref = ref_select(sets, n, os.cpu_count())
+        chn = ch.cpu().numpy().view(np.uint32)
+        estn = est.cpu().numpy()
+        out["reference"] = {"configs_costed_per_s": ref["configs_costed_per_s"],
+                            "us_per_batch": ref["us_per_request"] * R, "cores": ref["threads"],
+                            "sample": f"first {n} requests", "kind": "reference"}
+        out["digest_match"] = select_digest(chn, estn, n) == ref["digest"]
+    return out
 
 
 def run_deep(P, args, ws, rank, local, barrier):
@@ -403,6 +495,45 @@ def run_config5(horizon=240.0):
             "traces_identical": same, "points": pts,
             "note": "single-request decisions through the C ABI: each predict / round is one "
                     "launch + synchronisation, so tiny queues are launch-latency bound"}
+
+
+def run_config1():
+    """Config 1: the smallest bundled scenario,
+    reference.json (3 stages x 3 tiers), 1,000 requests, seed 1, policy
+    aragog, drain mode -- and the 3 x 4 variant adding tier "xl" (cost 9.0,
+    weight 0.4, 4 slots, service mu 1.6, sigma 0.25, floor 0.05) -- through
+    the reference's CPU router + scheduler (sim_trace_ref) and the same
+    sources relinked with the GPU adapter (sim_trace_gpu): wall time of the
+    run and trace identity."""
+    ref_bin, gpu_bin = os.path.join(INTEG, "sim_trace_ref"), os.path.join(INTEG, "sim_trace_gpu")
+    scen = os.path.join(INTEG, "proj", "scenarios", "reference.json")
+    if not (os.path.exists(ref_bin) and os.path.exists(gpu_bin) and os.path.exists(scen)):
+        return None
+    pts = []
+    with tempfile.TemporaryDirectory() as td:
+        base = json.load(open(scen))
+        xl = json.loads(json.dumps(base))
+        xl["name"] = "reference_xl"
+        xl["models"].append({"name": "xl", "cost": 9.0, "slot_throughput": 0.4})
+        xl["engines"].append({"model": "xl", "slots": 4, "service": {"mu": 1.6, "sigma": 0.25, "floor": 0.05}})
+        xl_path = os.path.join(td, "reference_xl.json")
+        json.dump(xl, open(xl_path, "w"))
+        for name, path in (("reference 3x3", scen), ("reference_xl 3x4", xl_path)):
+            row = {"name": name}
+            outs = []
+            for kind, b in (("reference", ref_bin), ("gpu", gpu_bin)):
+                out = os.path.join(td, f"{kind}_{len(pts)}.jsonl")
+                r = subprocess.run([b, path, "aragog", out, "--requests", "1000", "--seed", "1"],
+                                   capture_output=True, text=True, check=True)
+                j = json.loads(r.stdout.strip().splitlines()[-1])
+                row[kind] = {"rounds": j["rounds"], "requests": j["requests"], "wall_s": j["wall_s"],
+                             "rounds_per_s": j["rounds_per_s"], "gpu_launches": j["gpu_launches"]}
+                outs.append(open(out, "rb").read())
+            row["identical"] = outs[0] == outs[1]
+            pts.append(row)
+    return {"workload": "config1: reference.json (3x3) and its 3x4 xl variant, 1000 requests, seed 1, "
+                        "aragog policy, drain mode; reference build vs the GPU-adapter build",
+            "points": pts}
 
 
 def run_ours(args):
@@ -531,7 +662,23 @@ def run_ours(args):
                  "evaluations_per_request": float((cres.search_evals + cres.verify_evals)
                                                   .double().mean().item()),
                  "viable_per_request": float(cres.n_viable.double().mean().item())}
+        csel = None
+        if not args.no_select:
+            nv = cres.n_viable.to(torch.int64)
+            cmask = torch.arange(cres.viable.shape[1], device=dev_t)[None, :] < nv[:, None]
+            cmem = cres.viable[cmask].contiguous()
+            coffs = torch.zeros(REQUESTS_PER_GPU + 1, dtype=torch.int64, device=dev_t)
+            coffs[1:] = torch.cumsum(nv, 0)
+            csel = run_select(P, dev, "viable", cmem, coffs, int(coffs[-1]), stream, flush, barrier,
+                              rank == 0 and not args.no_cpu_baseline)
+            del cmem, coffs, cmask
         del pred, cres
+    select = None
+    if not args.no_select:
+        select = run_select(P, dev, "exhaustive", out["indices"], out["offsets"], total_members, stream,
+                            flush, barrier, rank == 0 and not args.no_cpu_baseline)
+        if chain and csel:
+            select["viable_sets"] = csel
     # the learned router: per-configuration linear
     # heads, the contraction emb . heads^T on tcgen05 with the threshold fused
     # into the epilogue; synthetic bf16 embeddings / heads (no reference)
@@ -632,6 +779,7 @@ def run_ours(args):
                                                             "device_p99_us", "rounds",
                                                             "by_free_slots")}}
     deep = None if args.no_deep else run_deep(P, args, ws, rank, local, barrier)
+    config1 = run_config1() if rank == 0 and not args.no_config5 else None
     config5 = run_config5() if rank == 0 and not args.no_config5 else None
     clk = clocks.stop()
 
@@ -679,8 +827,8 @@ def run_ours(args):
     # 1,500-character stdout tail keeps it) the compact summary of every leg
     line["detail"] = {"kernel_share": kernel_share, "members_per_step": total_members,
                       "sched": sched, "deep": deep, "noisy": noisy, "linear": linear,
-                      "chain": chain, "config5": config5}
-    line["summary"] = summarize(line, sched, deep, noisy, linear, chain, config5)
+                      "chain": chain, "select": select, "config1": config1, "config5": config5}
+    line["summary"] = summarize(line, sched, deep, noisy, linear, chain, config5, select, config1)
     print(json.dumps(line))
     if ws > 1:
         torch.distributed.destroy_process_group()
@@ -690,7 +838,7 @@ def _r(x, nd=3):
     return None if x is None else float(f"{x:.{nd}g}")
 
 
-def summarize(line, sched, deep, noisy, linear, chain, config5):
+def summarize(line, sched, deep, noisy, linear, chain, config5, select=None, config1=None):
     """One short record per leg (kept whole in the driver's stdout tail)."""
     out = {"route_configs_per_s": _r(line["value"]), "route_e2e": _r(line["e2e"]["value"]),
            "route_kernel_frac": _r(line["roofline"]["frac"])}
@@ -714,6 +862,19 @@ def summarize(line, sched, deep, noisy, linear, chain, config5):
                          "tensor_frac": _r(linear["roofline"]["frac"])}
     if chain:
         out["chain_requests_per_s"] = _r(chain["requests_per_s"])
+    if select:
+        out["select_us"] = {"exhaustive": _r(select["us_per_batch"]),
+                            "frac": _r(select["roofline"]["frac"]),
+                            "ref": _r((select.get("reference") or {}).get("us_per_batch")),
+                            "match": select.get("digest_match")}
+        vs = select.get("viable_sets")
+        if vs:
+            out["select_us"]["viable"] = _r(vs["us_per_batch"])
+            out["select_us"]["viable_ref"] = _r((vs.get("reference") or {}).get("us_per_batch"))
+            out["select_us"]["viable_match"] = vs.get("digest_match")
+    if config1:
+        out["config1"] = [[p["name"], p["identical"], _r(p["gpu"]["wall_s"]), _r(p["reference"]["wall_s"])]
+                          for p in config1["points"]]
     if config5:
         out["config5"] = {"identical": config5["traces_identical"],
                           "rounds_per_s": [[p["rate"], _r(p["gpu"]["rounds_per_s"]),
@@ -739,6 +900,25 @@ def spawn_ranks(args):
     os.execv(sys.executable, cmd)
 
 
+def spawn_selftest():
+    """`bench.py --gpus N --spawn-selftest`: the ranks spawn_ranks launched
+    meet in one process group (gloo, CPU) and rank 0 prints the world it saw."""
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if ws > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"n_gpus": ws, "ranks_joined": int(t.item()),
+                          "launcher": "torchrun" if "TORCHELASTIC_RUN_ID" in os.environ else "none"}))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -755,10 +935,16 @@ def main():
     ap.add_argument("--no-noisy", action="store_true")
     ap.add_argument("--no-chain", action="store_true")
     ap.add_argument("--no-linear", action="store_true")
+    ap.add_argument("--no-select", action="store_true")
     ap.add_argument("--no-ubench", action="store_true",
                     help="skip the PCIe / absorb-rate microbenchmarks (e.g. under ncu)")
+    ap.add_argument("--spawn-selftest", action="store_true",
+                    help="launcher check on CPU: ranks join a gloo group and rank 0 reports the world")
     args = ap.parse_args()
     spawn_ranks(args)
+    if args.spawn_selftest:
+        spawn_selftest()
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -342,11 +342,34 @@ typedef struct {
  * set (e.g. ag_route_enumerate's indices); chosen [R] (device) receives the
  * canonical index, est [R] (device, optional) its estimate_completion.
  * Static: minimum (static cost, index).  Runtime: minimum (estimate, static
- * cost, index), the reference's strict '<' scan over the cost-sorted list. */
+ * cost, index), the reference's strict '<' scan over the cost-sorted list.
+ * Fully asynchronous on the context stream (the task plan is built on the
+ * device); the reference's ValidationErrors -- an empty set, a member tier
+ * missing from the load context -- are latched on the device and returned by
+ * the next ag_ctx_synchronize. */
 int ag_select_per_input(ag_ctx* ctx, const uint32_t* members,
                         const uint64_t* offsets, int32_t n_requests,
                         int32_t kind, const ag_load* load, uint32_t* chosen,
                         double* est);
+
+/* ---- configuration-space sharding (config 4) ---------- */
+/* Per-shard record of select_per_input_config over this rank's canonical
+ * index range: records [R][4] u64 (device) = {member count, estimate (f64
+ * bits), static cost (f64 bits), canonical index} of the shard's minimum
+ * (estimate, static cost, index); an empty shard gives {0, +inf, +inf, ~0}.
+ * Asynchronous on the context stream (no host round trip), so the records
+ * can feed one NCCL all-gather directly. */
+int ag_shard_records(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets,
+                     int32_t n_requests, int32_t kind, const ag_load* load,
+                     uint64_t* records);
+/* Merge of the all-gathered records gathered [world][R][4] (device): per
+ * request the global member count total[R], the members of shards before
+ * `rank` before[R] (this rank's offset into the request's global list), and
+ * the whole-space choice best_index / best_est / best_cost [R] = the minimum
+ * of the shard minima.  Every output may be NULL.  Asynchronous. */
+int ag_merge_records(ag_ctx* ctx, const uint64_t* gathered, int32_t world, int32_t rank,
+                     int32_t n_requests, uint64_t* total, uint64_t* before,
+                     uint64_t* best_index, double* best_est, double* best_cost);
 
 /* select_per_input_config(accurate, space, kind, load) (workload.cpp:149-176)
  * for a batch of host AccurateSets, end to end on the device: every set's

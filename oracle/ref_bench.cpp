@@ -17,6 +17,19 @@
 //   ref_bench sched <requests> <beam> <rounds> <seed> <exhaustive:0|1>
 //       config-3 rounds: beam_schedule p50/p99 on one core (the scheduler is
 //       serial per round).
+//   ref_bench select <n> <m> <requests> <threads> <seed> <sets:exhaustive|viable>
+//       the per-stage re-cost + argmin: select_per_input_config(set, space,
+//       kPerInputRuntimeCost, &ctx) (workload.cpp:149-176) for every request,
+//       spread over threads with parallel_for.  The member lists are built
+//       before the timed region (the accurate set through at_index +
+//       AccurateSet::contains, or the predictor's ViableSet); timed per
+//       request: the sort by (static_cost, models) of members_by_cost
+//       (workload.cpp:32-42, restated: it is in an anonymous namespace) and
+//       the strict '<' scan over estimate_completion (workload.cpp:129-147,
+//       165-175, called as is).  Load context: occupancy 4, queued_ahead
+//       i % 3, 8 slots, ServiceTimeModel{mu -0.3 + 0.35 i, sigma 0.25,
+//       floor 0.05} per tier i.  Prints the digest of (chosen index, estimate
+//       bits) in request order.
 
 #include <algorithm>
 #include <array>
@@ -261,11 +274,83 @@ int run_sched(std::size_t inflight, int beam, int rounds, std::uint64_t seed, bo
   return 0;
 }
 
+int run_select(int n, int m, std::size_t requests, int threads, std::uint64_t seed,
+               bool exhaustive) {
+  WorkflowGraph g = chain_graph(n);
+  ModelCatalog cat = geometric_catalog(m);
+  ConfigSpace space(g, cat);
+  AccuracyGenParams ap;
+  AccuracyTable table = generate_accuracy_table(space, ap, requests, seed);
+  OracleRouter oracle(table, 0.002);
+  ConfigPredictor predictor(space, oracle);
+  std::vector<ServiceTimeModel::Params> sp(m);
+  for (int i = 0; i < m; ++i) sp[i] = {-0.3 + 0.35 * i, 0.25, 0.05};
+  ServiceTimeModel service(sp);
+  RuntimeCostContext ctx;
+  ctx.service = &service;
+  for (int i = 0; i < m; ++i) {
+    ctx.occupancy.push_back(4);
+    ctx.queued_ahead.push_back(i % 3);
+    ctx.slots.push_back(8);
+  }
+  std::vector<std::vector<Configuration>> sets(requests);
+  parallel_for(requests, threads, [&](std::size_t id) {
+    if (exhaustive) {
+      for (std::uint64_t i = 0; i < space.size(); ++i) {
+        Configuration c = space.at_index(i);
+        if (table.accurate(id, c)) sets[id].push_back(std::move(c));
+      }
+    } else {
+      sets[id] = predictor.predict(id, std::numeric_limits<double>::infinity()).viable.configs;
+    }
+  });
+  std::uint64_t costed = 0;
+  for (const auto& v : sets) costed += v.size();
+  std::vector<std::uint64_t> chosen(requests, 0);
+  std::vector<double> est(requests, 0.0);
+  auto t0 = Clock::now();
+  parallel_for(requests, threads, [&](std::size_t id) {
+    std::vector<Configuration> members = sets[id];  // members_by_cost copies its input
+    std::sort(members.begin(), members.end(), [&](const Configuration& a, const Configuration& b) {
+      double ca = space.static_cost(a), cb = space.static_cost(b);
+      if (ca != cb) return ca < cb;
+      return a.models < b.models;
+    });
+    std::size_t best = 0;
+    double best_est = estimate_completion(ctx, members[0]);
+    for (std::size_t i = 1; i < members.size(); ++i) {
+      double e = estimate_completion(ctx, members[i]);
+      if (e < best_est) {
+        best = i;
+        best_est = e;
+      }
+    }
+    chosen[id] = space.index_of(members[best]);
+    est[id] = best_est;
+  });
+  auto t1 = Clock::now();
+  double dt = secs(t0, t1);
+  std::uint64_t digest = 0x5eed;
+  for (std::size_t r = 0; r < requests; ++r) {
+    std::uint64_t bits;
+    std::memcpy(&bits, &est[r], 8);
+    digest = rng::mix({digest, chosen[r], bits});
+  }
+  std::printf(
+      "{\"mode\":\"select\",\"n\":%d,\"m\":%d,\"requests\":%zu,\"sets\":\"%s\","
+      "\"threads\":%d,\"seconds\":%.6f,\"configs_costed\":%llu,\"configs_costed_per_s\":%.6e,"
+      "\"us_per_request\":%.6f,\"digest\":\"%016llx\"}\n",
+      n, m, requests, exhaustive ? "exhaustive" : "viable", threads, dt,
+      (unsigned long long)costed, (double)costed / dt, dt * 1e6 / (double)requests,
+      (unsigned long long)digest);
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
   if (argc < 2) {
-    std::fprintf(stderr, "usage: ref_bench route|predict|sched ...\n");
+    std::fprintf(stderr, "usage: ref_bench route|predict|sched|select ...\n");
     return 2;
   }
   std::string mode = argv[1];
@@ -274,6 +359,12 @@ int main(int argc, char** argv) {
       return run_sched(static_cast<std::size_t>(std::atoll(argv[2])), std::atoi(argv[3]),
                        std::atoi(argv[4]), static_cast<std::uint64_t>(std::atoll(argv[5])),
                        std::atoi(argv[6]) != 0);
+    }
+    if (mode == "select" && argc >= 8) {
+      return run_select(std::atoi(argv[2]), std::atoi(argv[3]),
+                        static_cast<std::size_t>(std::atoll(argv[4])), std::atoi(argv[5]),
+                        static_cast<std::uint64_t>(std::atoll(argv[6])),
+                        std::strcmp(argv[7], "exhaustive") == 0);
     }
     if ((mode == "route" || mode == "predict") && argc >= 8) {
       return run_route(std::atoi(argv[2]), std::atoi(argv[3]),

@@ -80,6 +80,21 @@ Launch::~Launch() {
 
 using agb::fail;
 
+namespace agb {
+// Errors latched on the device by asynchronous entry points (bit 0: a member
+// uses a tier the estimator context lacks, workload.cpp:140-142; bit 1: an
+// empty accurate set, workload.cpp:151-156); the stream is synchronised.
+int take_async_status(ag_ctx* c) {
+  if (!c->async_status.p) return AG_OK;
+  int32_t st = 0;
+  AG_CUDA(cudaMemcpy(&st, c->async_status.p, 4, cudaMemcpyDeviceToHost));
+  if (!st) return AG_OK;
+  AG_CUDA(cudaMemset(c->async_status.p, 0, 4));
+  if (st & 2) return fail(AG_ERR_VALIDATION, "accurate set is empty");
+  return fail(AG_ERR_VALIDATION, "estimator context missing a model tier");
+}
+}  // namespace agb
+
 extern "C" {
 
 const char* ag_last_error(void) { return agb::g_error.c_str(); }
@@ -187,7 +202,7 @@ int ag_ctx_create(const ag_space* space, int device, ag_ctx** out) {
   if (e != cudaSuccess || count == 0)
     return fail(AG_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
   if (device < 0 || device >= count) return fail(AG_ERR_VALIDATION, "device out of range");
-  AG_CUDA(cudaSetDevice(device));
+  agb::DeviceGuard device_guard(device);
   ag_ctx* c = new ag_ctx();
   c->space = space;
   c->device = device;
@@ -196,8 +211,8 @@ int ag_ctx_create(const ag_space* space, int device, ag_ctx** out) {
 }
 
 void ag_ctx_destroy(ag_ctx* c) {
+  agb::DeviceGuard device_guard(c ? c->device : -1);
   if (!c) return;
-  cudaSetDevice(c->device);
   for (auto& r : c->prof) {
     cudaEventDestroy(r.start);
     cudaEventDestroy(r.stop);
@@ -215,14 +230,16 @@ int ag_ctx_set_stream(ag_ctx* c, void* stream) {
 }
 
 int ag_ctx_synchronize(ag_ctx* c) {
+  agb::DeviceGuard device_guard(c ? c->device : -1);
   if (!c) return fail(AG_ERR_VALIDATION, "ctx is null");
   AG_CUDA(cudaStreamSynchronize(c->stream));
-  return AG_OK;
+  return agb::take_async_status(c);
 }
 
 uint64_t ag_ctx_launch_count(const ag_ctx* c) { return c ? c->launches : 0; }
 
 int ag_ctx_profile_begin(ag_ctx* c) {
+  agb::DeviceGuard device_guard(c ? c->device : -1);
   if (!c) return fail(AG_ERR_VALIDATION, "ctx is null");
   for (auto& r : c->prof) {
     c->event_pool.push_back(r.start);
@@ -234,6 +251,7 @@ int ag_ctx_profile_begin(ag_ctx* c) {
 }
 
 int ag_ctx_profile_end(ag_ctx* c, double* ms, uint64_t* launches) {
+  agb::DeviceGuard device_guard(c ? c->device : -1);
   if (!c) return fail(AG_ERR_VALIDATION, "ctx is null");
   c->profiling = false;
   AG_CUDA(cudaStreamSynchronize(c->stream));
@@ -276,6 +294,7 @@ int ag_device_free(void* p) {
 
 int ag_route_enumerate(ag_ctx* ctx, const ag_truth* truth, const ag_router* router,
                        uint64_t begin, uint64_t end, uint32_t flags, const ag_route_out* out) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx) return fail(AG_ERR_VALIDATION, "ctx is null");
   return agb::route_enumerate(ctx, truth, router, begin, end, flags, out);
 }
@@ -334,6 +353,7 @@ extern "C" {
 // (accuracy.cpp:227-238 + workload.cpp:149-176); only the choice comes back.
 int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* th, int32_t kind, const ag_load* load,
                              uint32_t* chosen, double* est) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !th || !chosen) return fail(AG_ERR_VALIDATION, "null argument");
   const int R = th->n_requests;
   if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
@@ -367,13 +387,14 @@ int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* th, int32_t kind, cons
   AG_CUDA(cudaMemcpyAsync(chosen, d_chosen, 4 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));
   if (est) AG_CUDA(cudaMemcpyAsync(est, d_est, 8 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));
   AG_CUDA(cudaStreamSynchronize(ctx->stream));
-  return AG_OK;
+  return agb::take_async_status(ctx);
 }
 
 int ag_route_enumerate_host(ag_ctx* ctx, const ag_truth* th, const ag_router* router,
                             uint64_t begin, uint64_t end, uint32_t flags, uint64_t* counts,
                             uint64_t* offsets, uint32_t* indices, uint64_t capacity,
                             uint64_t* total) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !th || !offsets || (th->n_requests > 0 && !counts))
     return fail(AG_ERR_VALIDATION, "null argument");
   const int R = th->n_requests;

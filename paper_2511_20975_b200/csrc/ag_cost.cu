@@ -22,6 +22,7 @@
 // SMs; small requests are one task each.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <vector>
 
@@ -31,7 +32,8 @@ namespace agb {
 namespace {
 
 constexpr int kCostWarps = 8;
-constexpr uint64_t kTask = 1 << 16;
+constexpr uint64_t kTask = 1 << 16;     // members per task (at least)
+constexpr uint64_t kTaskCap = 1 << 20;  // tasks per call beyond one per request
 constexpr uint64_t kPrefixMax = 1u << 22;  // prefix-table entries (64 MB)
 
 struct Key {
@@ -47,15 +49,16 @@ __device__ __forceinline__ bool key_less(double e1, double c1, uint32_t i1, doub
 struct CostArgs {
   SpaceDev sp;
   const uint32_t* members;
-  int n_tasks;
-  const uint64_t* t_begin;  // [n_tasks]
-  const uint64_t* t_end;
+  const uint64_t* offsets;      // [R+1] member CSR
   int kind;                     // 0 static, 1 runtime
   double term[kMaxModels + 1];  // per-tier estimate term (NaN: tier missing)
   double cost[kMaxModels + 1];
-  Key* task_best;               // [n_tasks]
+  Key* task_best;               // [tasks]
   int R;
-  const int32_t* r_task;        // [R+1] task range per request
+  int32_t* r_task;              // [R+1] task range per request (k_cost_plan)
+  uint64_t* tsize;              // members per task (k_cost_plan)
+  uint64_t* rec;                // [R][4] shard records (ag_shard_records) or null
+  int allow_empty;              // shard records: an empty shard is not an error
   uint32_t* chosen;
   double* est;
   int32_t* status;
@@ -66,9 +69,8 @@ struct CostArgs {
 };
 
 // Stage 0: prefix folds (estimate_completion / static_cost, left to right)
-__global__ void __launch_bounds__(256) k_cost_prefix(const CostArgs* __restrict__ Ap, uint64_t n_pre,
+__global__ void __launch_bounds__(256) k_cost_prefix(const __grid_constant__ CostArgs A, uint64_t n_pre,
                                                      double2* __restrict__ out) {
-  const CostArgs& A = *Ap;
   const uint64_t q = (uint64_t)blockIdx.x * 256 + threadIdx.x;
   if (q >= n_pre) return;
   const uint32_t m = (uint32_t)A.sp.m;
@@ -87,11 +89,60 @@ __global__ void __launch_bounds__(256) k_cost_prefix(const CostArgs* __restrict_
   out[q] = make_double2(e, c);
 }
 
+// The task plan on the device (no host round trip): request r owns tasks
+// [r_task[r], r_task[r+1]), one per tsize members (kTask, or more when the
+// batch holds over kTaskCap * kTask members, so at most R + kTaskCap tasks);
+// an empty set latches "accurate set is empty" (workload.cpp:151-156) and
+// gets no task.
+__global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ CostArgs A) {
+  __shared__ int32_t s_wsum[32];
+  __shared__ int32_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  const uint64_t total = A.offsets[A.R] - A.offsets[0];
+  const uint64_t tq = (total + kTaskCap - 1) / kTaskCap;
+  const uint64_t ts = tq > kTask ? tq : kTask;
+  if (tid == 0) *A.tsize = ts;
+  __syncthreads();
+  for (int base = 0; base < A.R; base += 1024) {
+    const int r = base + tid;
+    int32_t nt = 0;
+    if (r < A.R) {
+      const uint64_t len = A.offsets[r + 1] - A.offsets[r];
+      if (len == 0 && !A.allow_empty) atomicOr(A.status, 2);
+      nt = (int32_t)((len + ts - 1) / ts);
+    }
+    int32_t x = nt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int32_t v = s_wsum[lane], z = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      s_wsum[lane] = z - v;
+    }
+    __syncthreads();
+    const int32_t carry = s_carry;
+    if (r < A.R) A.r_task[r] = carry + s_wsum[w] + x - nt;
+    __syncthreads();
+    if (tid == 1023) s_carry = carry + s_wsum[31] + x;
+    __syncthreads();
+  }
+  if (tid == 0) A.r_task[A.R] = s_carry;
+}
+
 // SFX = N - k suffix digits per member (1..4 specialised; 0 = runtime, <= 16:
 // M^N <= 2^32 and M^k <= kPrefixMax leave at most 16).
 template <int SFX>
-__global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const CostArgs* __restrict__ Ap) {
-  const CostArgs& A = *Ap;
+__global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_constant__ CostArgs A) {
   __shared__ double s_term[kMaxModels + 1], s_cost[kMaxModels + 1];
   const int m_ = A.sp.m;
   for (int i = threadIdx.x; i < m_; i += blockDim.x) {
@@ -100,10 +151,18 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const CostArgs* 
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int t = blockIdx.x * kCostWarps + (threadIdx.x >> 5);
-  if (t >= A.n_tasks) return;
-  const uint64_t b0 = A.t_begin[t];
-  const uint32_t len = (uint32_t)(A.t_end[t] - b0);  // <= kTask
+  const int n_tasks = A.r_task[A.R];
+  const uint64_t ts = *A.tsize;
+  // persistent warps over the tasks (their number is only known on the device)
+  for (int t = blockIdx.x * kCostWarps + (threadIdx.x >> 5); t < n_tasks; t += gridDim.x * kCostWarps) {
+  int r = 0;  // the task's request: last r with r_task[r] <= t (binary search)
+  for (int lo = 0, hi = A.R; lo < hi;) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (A.r_task[mid] <= t) r = mid, lo = mid; else hi = mid - 1;
+  }
+  const uint64_t b0 = A.offsets[r] + (uint64_t)(t - A.r_task[r]) * ts;
+  const uint64_t rest = A.offsets[r + 1] - b0;
+  const uint32_t len = (uint32_t)(rest < ts ? rest : ts);
   const uint32_t* mem = A.members + b0;
   const int sfx = SFX > 0 ? SFX : A.sp.n - A.k;
   const uint32_t m = (uint32_t)m_, mk = A.mk;
@@ -158,12 +217,12 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const CostArgs* 
     const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (key_less(oe, oc, oi, be, bc, bi)) be = oe, bc = oc, bi = oi;
   }
-  if (__any_sync(0xffffffffu, missing) && lane == 0) atomicExch(A.status, AG_ERR_VALIDATION);
+  if (__any_sync(0xffffffffu, missing) && lane == 0) atomicOr(A.status, 1);
   if (lane == 0) A.task_best[t] = Key{be, bc, bi};
+  }
 }
 
-__global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const CostArgs* __restrict__ Ap) {
-  const CostArgs& A = *Ap;
+__global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const __grid_constant__ CostArgs A) {
   const int lane = threadIdx.x & 31;
   const int r = blockIdx.x * kCostWarps + (threadIdx.x >> 5);
   if (r >= A.R) return;
@@ -181,9 +240,47 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const CostArgs*
     if (key_less(oe, oc, oi, be, bc, bi)) be = oe, bc = oc, bi = oi;
   }
   if (lane == 0) {
-    A.chosen[r] = bi;
+    if (A.chosen) A.chosen[r] = bi;
     if (A.est) A.est[r] = be;
+    if (A.rec) {
+      // {count, estimate, static cost, index}; an empty shard carries +inf keys
+      const uint64_t cnt = A.offsets[r + 1] - A.offsets[r];
+      A.rec[4 * r] = cnt;
+      A.rec[4 * r + 1] = (uint64_t)__double_as_longlong(cnt ? be : INFINITY);
+      A.rec[4 * r + 2] = (uint64_t)__double_as_longlong(cnt ? bc : INFINITY);
+      A.rec[4 * r + 3] = cnt ? (uint64_t)bi : ~0ULL;
+    }
   }
+}
+
+// Merge of the all-gathered shard records [world][R][4] (rank order is
+// canonical order): per request the global member count, the members of the
+// shards before `rank` (this rank's global offset into the request's list),
+// and the lexicographic minimum of (estimate, static cost, index) over the
+// non-empty shards -- the whole-space select_per_input_config choice
+// (workload.cpp:149-176), since the minimum of shard minima is the minimum.
+__global__ void __launch_bounds__(256) k_merge_records(const uint64_t* __restrict__ g, int world, int rank, int R,
+                                                       uint64_t* total, uint64_t* before, uint64_t* best_idx,
+                                                       double* best_est, double* best_cost) {
+  const int r = blockIdx.x * 256 + threadIdx.x;
+  if (r >= R) return;
+  uint64_t tot = 0, bef = 0, bi = ~0ULL;
+  double be = INFINITY, bc = INFINITY;
+  for (int w = 0; w < world; ++w) {
+    const uint64_t* x = g + ((size_t)w * R + r) * 4;
+    const uint64_t cnt = x[0];
+    if (w < rank) bef += cnt;
+    tot += cnt;
+    if (!cnt) continue;
+    const double e = __longlong_as_double((long long)x[1]), c = __longlong_as_double((long long)x[2]);
+    const uint64_t i = x[3];
+    if (e < be || (e == be && (c < bc || (c == bc && i < bi)))) be = e, bc = c, bi = i;
+  }
+  if (total) total[r] = tot;
+  if (before) before[r] = bef;
+  if (best_idx) best_idx[r] = bi;
+  if (best_est) best_est[r] = be;
+  if (best_cost) best_cost[r] = bc;
 }
 
 }  // namespace
@@ -191,38 +288,27 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const CostArgs*
 
 using agb::fail;
 
-extern "C" int ag_select_per_input(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets,
-                                   int32_t n_requests, int32_t kind, const ag_load* load,
-                                   uint32_t* chosen, double* est) {
-  if (!ctx || !members || !offsets || !chosen) return fail(AG_ERR_VALIDATION, "null argument");
+namespace agb {
+namespace {
+
+// select_per_input_config over a member CSR, asynchronous: the chosen index /
+// estimate per request, or (rec) the 32-byte shard record per request
+int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, int32_t n_requests,
+                int32_t kind, const ag_load* load, uint32_t* chosen, double* est, uint64_t* rec) {
+  if (!ctx || !members || !offsets || (!chosen && !rec)) return fail(AG_ERR_VALIDATION, "null argument");
   if (kind != AG_POLICY_PER_INPUT_STATIC && kind != AG_POLICY_PER_INPUT_RUNTIME_COST)
     return fail(AG_ERR_VALIDATION, "per-input selection needs a per-input policy kind");
   if (kind == AG_POLICY_PER_INPUT_RUNTIME_COST && !load)
     return fail(AG_ERR_VALIDATION, "runtime-cost selection needs a load context");
   const ag_space* sp = ctx->space;
-  if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N <= 2^32 and N <= 32");
+  if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N < 2^32 and N <= 32");
   if (n_requests <= 0) return n_requests == 0 ? AG_OK : fail(AG_ERR_VALIDATION, "negative request count");
   cudaStream_t st = ctx->stream;
   const int R = n_requests;
-  // task table from the request offsets (one slice of <= kTask members each)
-  std::vector<uint64_t> off(R + 1);
-  AG_CUDA(cudaMemcpyAsync(off.data(), offsets, 8 * (size_t)(R + 1), cudaMemcpyDeviceToHost, st));
-  AG_CUDA(cudaStreamSynchronize(st));
-  std::vector<uint64_t> tb, te;
-  std::vector<int32_t> rt(R + 1, 0);
-  for (int r = 0; r < R; ++r) {
-    if (off[r + 1] <= off[r]) return fail(AG_ERR_VALIDATION, "accurate set is empty");
-    for (uint64_t b = off[r]; b < off[r + 1]; b += agb::kTask) {
-      tb.push_back(b);
-      te.push_back(std::min(off[r + 1], b + agb::kTask));
-    }
-    rt[r + 1] = (int32_t)tb.size();
-  }
-  const int T = (int)tb.size();
   agb::CostArgs A;
   A.sp = sp->dev();
   A.members = members;
-  A.n_tasks = T;
+  A.offsets = offsets;
   A.kind = kind == AG_POLICY_PER_INPUT_RUNTIME_COST ? 1 : 0;
   for (int i = 0; i <= agb::kMaxModels; ++i) {
     A.term[i] = 0.0;
@@ -244,6 +330,8 @@ extern "C" int ag_select_per_input(ag_ctx* ctx, const uint32_t* members, const u
   A.R = R;
   A.chosen = chosen;
   A.est = est;
+  A.rec = rec;
+  A.allow_empty = rec != nullptr;
   // prefix table: the largest k <= N - 1 with M^k <= kPrefixMax
   {
     int k = 0;
@@ -252,55 +340,91 @@ extern "C" int ag_select_per_input(ag_ctx* ctx, const uint32_t* members, const u
     uint64_t mk = 1;
     for (int a = k; a < sp->n; ++a) mk *= (uint64_t)sp->m;
     A.k = k;
-    A.mk = (uint32_t)mk;  // <= M^N <= 2^32 (gpu_ok); M^N == 2^32 needs k >= 1
+    A.mk = (uint32_t)mk;  // <= M^N < 2^32 (gpu_ok)
     A.div_mk = mk > 1 ? (~0ULL) / mk + 1 : 0;
     if (mk <= 1) return fail(AG_ERR_INTERNAL, "prefix table covers every digit");
     if (sp->n - k > 16) return fail(AG_ERR_INTERNAL, "more than 16 digits outside the prefix table");
   }
   uint64_t n_pre = 1;
   for (int a = 0; a < A.k; ++a) n_pre *= (uint64_t)sp->m;
+  // task bests: at most R + kTaskCap tasks (k_cost_plan sizes the tasks)
   int rc;
-  const size_t tbytes = (size_t)T * 16 + (size_t)(R + 1) * 4 + (size_t)T * sizeof(agb::Key) + 64;
-  if ((rc = ctx->cost_args.ensure(sizeof(A))) || (rc = ctx->cost_status.ensure(tbytes)) ||
-      (rc = ctx->cost_prefix.ensure(16 * n_pre)))
+  const size_t tcap = (size_t)R + agb::kTaskCap;
+  if (!ctx->async_status.p) {
+    if ((rc = ctx->async_status.ensure(16))) return rc;
+    AG_CUDA(cudaMemsetAsync(ctx->async_status.p, 0, 16, st));
+  }
+  if ((rc = ctx->cost_status.ensure((size_t)(R + 1) * 4 + 64)) ||
+      (rc = ctx->cost_tasks.ensure(tcap * sizeof(agb::Key))) || (rc = ctx->cost_prefix.ensure(16 * n_pre)))
     return rc;
   A.prefix = (const double2*)ctx->cost_prefix.p;
-  char* d = (char*)ctx->cost_status.p;
-  A.status = (int32_t*)d;
-  A.t_begin = (const uint64_t*)(d + 16);
-  A.t_end = A.t_begin + T;
-  A.r_task = (const int32_t*)(A.t_end + T);
-  A.task_best = (agb::Key*)(((uintptr_t)(A.r_task + R + 1) + 15) & ~(uintptr_t)15);
-  AG_CUDA(cudaMemsetAsync(d, 0, 16, st));
-  AG_CUDA(cudaMemcpyAsync((void*)A.t_begin, tb.data(), 8 * (size_t)T, cudaMemcpyHostToDevice, st));
-  AG_CUDA(cudaMemcpyAsync((void*)A.t_end, te.data(), 8 * (size_t)T, cudaMemcpyHostToDevice, st));
-  AG_CUDA(cudaMemcpyAsync((void*)A.r_task, rt.data(), 4 * (size_t)(R + 1), cudaMemcpyHostToDevice, st));
-  // the argument block (per-tier tables) is too large for kernel parameters
-  AG_CUDA(cudaMemcpyAsync(ctx->cost_args.p, &A, sizeof(A), cudaMemcpyHostToDevice, st));
-  const agb::CostArgs* dA = (const agb::CostArgs*)ctx->cost_args.p;
+  A.status = (int32_t*)ctx->async_status.p;
+  A.r_task = (int32_t*)ctx->cost_status.p;
+  A.tsize = (uint64_t*)((char*)ctx->cost_status.p + (((size_t)(R + 1) * 4 + 15) & ~(size_t)15));
+  A.task_best = (agb::Key*)ctx->cost_tasks.p;
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    agb::k_cost_prefix<<<(unsigned)((n_pre + 255) / 256), 256, 0, st>>>(dA, n_pre, (double2*)ctx->cost_prefix.p);
+    agb::k_cost_plan<<<1, 1024, 0, st>>>(A);
   }
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    const dim3 g((T + agb::kCostWarps - 1) / agb::kCostWarps), b(agb::kCostWarps * 32);
+    agb::k_cost_prefix<<<(unsigned)((n_pre + 255) / 256), 256, 0, st>>>(A, n_pre, (double2*)ctx->cost_prefix.p);
+  }
+  {
+    agb::Launch L(ctx, agb::K_COST_ARGMIN);
+    if (!ctx->cost_grid) {
+      int sms = 0, per_sm = 0;
+      AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+      AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agb::k_cost_tasks<0>, agb::kCostWarps * 32, 0));
+      ctx->cost_grid = std::max(1, sms * per_sm);
+    }
+    const dim3 g(ctx->cost_grid), b(agb::kCostWarps * 32);
     switch (sp->n - A.k) {
-      case 1: agb::k_cost_tasks<1><<<g, b, 0, st>>>(dA); break;
-      case 2: agb::k_cost_tasks<2><<<g, b, 0, st>>>(dA); break;
-      case 3: agb::k_cost_tasks<3><<<g, b, 0, st>>>(dA); break;
-      case 4: agb::k_cost_tasks<4><<<g, b, 0, st>>>(dA); break;
-      default: agb::k_cost_tasks<0><<<g, b, 0, st>>>(dA); break;
+      case 1: agb::k_cost_tasks<1><<<g, b, 0, st>>>(A); break;
+      case 2: agb::k_cost_tasks<2><<<g, b, 0, st>>>(A); break;
+      case 3: agb::k_cost_tasks<3><<<g, b, 0, st>>>(A); break;
+      case 4: agb::k_cost_tasks<4><<<g, b, 0, st>>>(A); break;
+      default: agb::k_cost_tasks<0><<<g, b, 0, st>>>(A); break;
     }
   }
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    agb::k_cost_reduce<<<(R + agb::kCostWarps - 1) / agb::kCostWarps, agb::kCostWarps * 32, 0, st>>>(dA);
+    agb::k_cost_reduce<<<(R + agb::kCostWarps - 1) / agb::kCostWarps, agb::kCostWarps * 32, 0, st>>>(A);
   }
   AG_CUDA(cudaGetLastError());
-  int32_t stv = 0;
-  AG_CUDA(cudaMemcpyAsync(&stv, d, 4, cudaMemcpyDeviceToHost, st));
-  AG_CUDA(cudaStreamSynchronize(st));
-  if (stv) return fail(AG_ERR_VALIDATION, "estimator context missing a model tier");
+  return AG_OK;
+}
+
+}  // namespace
+}  // namespace agb
+
+extern "C" int ag_select_per_input(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets,
+                                   int32_t n_requests, int32_t kind, const ag_load* load,
+                                   uint32_t* chosen, double* est) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
+  if (!chosen) return fail(AG_ERR_VALIDATION, "null argument");
+  return agb::select_impl(ctx, members, offsets, n_requests, kind, load, chosen, est, nullptr);
+}
+
+extern "C" int ag_shard_records(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets,
+                                int32_t n_requests, int32_t kind, const ag_load* load, uint64_t* records) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
+  if (!records) return fail(AG_ERR_VALIDATION, "null argument");
+  return agb::select_impl(ctx, members, offsets, n_requests, kind, load, nullptr, nullptr, records);
+}
+
+extern "C" int ag_merge_records(ag_ctx* ctx, const uint64_t* gathered, int32_t world, int32_t rank,
+                                int32_t n_requests, uint64_t* total, uint64_t* before, uint64_t* best_index,
+                                double* best_est, double* best_cost) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
+  if (!ctx || !gathered) return fail(AG_ERR_VALIDATION, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(AG_ERR_VALIDATION, "rank outside the world");
+  if (n_requests <= 0) return n_requests == 0 ? AG_OK : fail(AG_ERR_VALIDATION, "negative request count");
+  {
+    agb::Launch L(ctx, agb::K_COST_ARGMIN);
+    agb::k_merge_records<<<(n_requests + 255) / 256, 256, 0, ctx->stream>>>(gathered, world, rank, n_requests, total,
+                                                                          before, best_index, best_est, best_cost);
+  }
+  AG_CUDA(cudaGetLastError());
   return AG_OK;
 }

@@ -82,7 +82,8 @@ struct ag_ctx {
   agb::Scratch colmask;  // per-space last-digit masks (route 2-D path)
   agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
   bool hc_ready = false;
-  agb::Scratch cost_args, cost_status, cost_prefix;  // runtime-cost argmin
+  agb::Scratch cost_status, cost_tasks, cost_prefix;  // runtime-cost argmin: plan, task bests, prefix folds
+  int cost_grid = 0;                                  // k_cost_tasks blocks resident on the device
   int colmask_m = 0;
   // host-path staging
   agb::Scratch h_truth;
@@ -90,11 +91,34 @@ struct ag_ctx {
   agb::Scratch d_sel;        // select_per_input host path: chosen / estimate
   agb::Scratch wf_hits, wf_best;  // select_per_workflow: hit counts, block minima
   ag_sched* beam_cache = nullptr;  // session reused by stateless beam_schedule
+  // per-device launch configuration (cudaFuncSetAttribute and occupancy are
+  // per device, so they are cached per context, never per process)
+  bool scan_attr = false;    // k_request_scan<12>/<24> dynamic shared memory
+  int compact_resident = 0;  // k_route_compact blocks resident on the device
+  int linear_sms = 0;        // SM count; k_linear_score attributes set
+  // errors latched by asynchronous kernels (ag_select_per_input), reported
+  // by the next synchronising call on the context
+  agb::Scratch async_status;
   void* h_stage = nullptr;   // pinned staging for host-path uploads
   size_t h_stage_bytes = 0;
 };
 
 namespace agb {
+
+// Every entry point runs on its context's device and leaves the caller's
+// current device as it found it.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    int cur = 0;
+    if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 // Brackets one kernel launch with CUDA events on the context stream when the
 // live profile is enabled, and counts the launch.
@@ -117,5 +141,6 @@ int make_router(const ag_router* r, RouterDev* out);
 // host ag_truth -> device view in the context's staging buffer
 int upload_truth(ag_ctx* ctx, const ag_truth* host, ag_truth* dev);
 int ensure_host_stage(ag_ctx* ctx, size_t bytes);
+int take_async_status(ag_ctx* ctx);
 
 }  // namespace agb

@@ -409,6 +409,7 @@ using agb::fail;
 
 extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests, const ag_linear_heads* heads,
                                uint64_t begin, uint64_t end, uint32_t flags, const ag_route_out* out) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !heads || !out) return fail(AG_ERR_VALIDATION, "null argument");
   const ag_space* sp = ctx->space;
   if (!sp->gpu_ok) return fail(AG_ERR_VALIDATION, "GPU path needs M^N <= 2^32 and N <= 32");
@@ -475,7 +476,7 @@ extern "C" int ag_route_linear(ag_ctx* ctx, const void* emb, int32_t n_requests,
                                   agb::k_linear_score<4>, agb::k_linear_score<5>, agb::k_linear_score<6>,
                                   agb::k_linear_score<7>, agb::k_linear_score<8>};
     const lin_fn fn = fns[heads->dim / 16 - 1];
-    static int n_sms = 0;
+    int& n_sms = ctx->linear_sms;
     if (!n_sms) {
       for (int i = 0; i < 8; ++i)
         AG_CUDA(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -357,6 +357,7 @@ extern "C" {
 // ConfigPredictor ctor (predictor.cpp:158-163) -> build_chains (:107-131)
 int ag_predictor_create(ag_ctx* ctx, int chain_cap, uint64_t exhaustive_limit,
                         ag_predictor** out) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !out) return fail(AG_ERR_VALIDATION, "null argument");
   *out = nullptr;
   const ag_space* sp = ctx->space;
@@ -430,7 +431,10 @@ int ag_predictor_create(ag_ctx* ctx, int chain_cap, uint64_t exhaustive_limit,
   return AG_OK;
 }
 
-void ag_predictor_destroy(ag_predictor* p) { delete p; }
+void ag_predictor_destroy(ag_predictor* p) {
+  agb::DeviceGuard device_guard(p ? p->ctx->device : -1);
+  delete p;
+}
 
 int ag_predictor_info(const ag_predictor* p, int32_t* n_chains, int32_t* chain_len,
                       int32_t* exhaustive, int32_t* n_unique, uint64_t* chains) {
@@ -446,6 +450,7 @@ int ag_predictor_info(const ag_predictor* p, int32_t* n_chains, int32_t* chain_l
 // ConfigPredictor::predict (predictor.cpp:165-262) for a batch of requests
 int ag_predict(ag_predictor* p, const ag_truth* t, const ag_router* router,
                const double* budgets, double budget_all, const ag_predict_out* out) {
+  agb::DeviceGuard device_guard(p ? p->ctx->device : -1);
   if (!p || !t || !out || !out->viable || !out->n_viable)
     return fail(AG_ERR_VALIDATION, "null argument");
   ag_ctx* ctx = p->ctx;
@@ -496,6 +501,7 @@ int ag_predict_host(ag_predictor* p, const ag_truth* th, const ag_router* router
                     const double* budgets, double budget_all, uint32_t* viable,
                     int32_t viable_stride, int32_t* n_viable, int32_t* search_evals,
                     int32_t* verify_evals, double* router_time, uint8_t* truncated) {
+  agb::DeviceGuard device_guard(p ? p->ctx->device : -1);
   if (!p || !th || !viable || !n_viable || !router) return fail(AG_ERR_VALIDATION, "null argument");
   ag_ctx* ctx = p->ctx;
   const int R = th->n_requests;

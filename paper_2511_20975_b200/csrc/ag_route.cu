@@ -831,9 +831,9 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
-cudaError_t launch_request_scan(cudaStream_t s, const uint64_t* counts, uint64_t* offsets, int R, uint64_t capacity,
-                                uint32_t* overflow) {
-  static bool attr = false;
+cudaError_t launch_request_scan(ag_ctx* ctx, cudaStream_t s, const uint64_t* counts, uint64_t* offsets, int R,
+                                uint64_t capacity, uint32_t* overflow) {
+  bool& attr = ctx->scan_attr;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_request_scan<12>, cudaFuncAttributeMaxDynamicSharedMemorySize, 12 * 1024 * 8);
     if (e == cudaSuccess)
@@ -1060,11 +1060,10 @@ int make_router(const ag_router* r, RouterDev* out) {
 // sized to the device's resident capacity for this kernel.
 int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, const uint32_t* bitmap,
                    const uint64_t* offsets, uint32_t* indices, uint64_t capacity) {
-  static int resident = 0;  // blocks per device (SMs x blocks per SM)
+  int& resident = ctx->compact_resident;  // blocks per device (SMs x blocks per SM)
   if (!resident) {
-    int dev = 0, sms = 0, per_sm = 0;
-    AG_CUDA(cudaGetDevice(&dev));
-    AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int sms = 0, per_sm = 0;
+    AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
     AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_route_compact, kThreads, 0));
     resident = std::max(1, sms * per_sm);
   }
@@ -1160,7 +1159,7 @@ int route_enumerate(ag_ctx* ctx, const ag_truth* t, const ag_router* r, uint64_t
   } else {
     AG_CUDA(cudaMemsetAsync(out->counts, 0, (size_t)R * 8, s));
     Launch L(ctx, K_REQUEST_SCAN);
-    AG_CUDA(launch_request_scan(s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
+    AG_CUDA(launch_request_scan(ctx, s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
     AG_CUDA(cudaGetLastError());
     return AG_OK;
   }
@@ -1195,7 +1194,7 @@ int finish_enumerate(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin,
   }
   {
     Launch L(ctx, K_REQUEST_SCAN);
-    AG_CUDA(launch_request_scan(s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
+    AG_CUDA(launch_request_scan(ctx, s, out->counts, offsets, R, out->indices ? out->capacity : ~0ULL, out->overflow));
   }
   if (out->indices) {
     const int rc = launch_compact(ctx, R, W, C, begin, bitmap, offsets, out->indices, out->capacity);

@@ -1886,6 +1886,7 @@ using agb::fail;
 extern "C" {
 
 int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_sched** out) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !out) return fail(AG_ERR_VALIDATION, "null argument");
   *out = nullptr;
   const ag_space* sp = ctx->space;
@@ -1939,9 +1940,13 @@ int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_
   return AG_OK;
 }
 
-void ag_sched_destroy(ag_sched* s) { delete s; }
+void ag_sched_destroy(ag_sched* s) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  delete s;
+}
 
 int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || !q) return fail(AG_ERR_VALIDATION, "null argument");
   ag_ctx* ctx = s->ctx;
   const int R = q->n_requests;
@@ -2013,6 +2018,7 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
 }
 
 int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s) return fail(AG_ERR_VALIDATION, "null argument");
   for (int i = 0; i < n; ++i) {
     const int slot = slots[i];
@@ -2033,6 +2039,7 @@ int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
 }
 
 int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || slot < 0 || slot >= s->cap || !s->live[slot]) return fail(AG_ERR_VALIDATION, "bad slot");
   const int N = s->N;
   if (agent < 0 || agent >= N || s->stages[(size_t)slot * N + agent] != AG_STAGE_INFLIGHT)
@@ -2055,11 +2062,13 @@ int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent) {
 
 int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width, ag_assignment* out,
                    ag_triple* triples, int32_t triples_cap, int32_t* occupancy) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s) return fail(AG_ERR_VALIDATION, "null argument");
   return agb::run_round(s, engines, beam_width, nullptr, out, triples, triples_cap, occupancy);
 }
 
 int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s) return fail(AG_ERR_VALIDATION, "null argument");
   const int N = s->N;
   for (int i = 0; i < n; ++i) {
@@ -2092,6 +2101,7 @@ int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
 }
 
 int ag_sched_queued_ahead(ag_sched* s, int32_t* out) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || !out) return fail(AG_ERR_VALIDATION, "null argument");
   ag_ctx* ctx = s->ctx;
   cudaStream_t st = ctx->stream;
@@ -2126,6 +2136,7 @@ int ag_sched_queued_ahead(ag_sched* s, int32_t* out) {
 }
 
 int ag_sched_round_timing(ag_sched* s, uint64_t* ns) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || !ns) return fail(AG_ERR_VALIDATION, "null argument");
   AG_CUDA(cudaMemcpyAsync(ns, (char*)s->d_status.p + 32, 128, cudaMemcpyDeviceToHost, s->ctx->stream));
   AG_CUDA(cudaStreamSynchronize(s->ctx->stream));
@@ -2135,6 +2146,7 @@ int ag_sched_round_timing(ag_sched* s, uint64_t* ns) {
 double ag_sched_last_round_us(const ag_sched* s) { return s ? s->last_round_us : 0.0; }
 
 int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap, int64_t* n) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || slot < 0 || slot >= s->cap || !s->live[slot]) return fail(AG_ERR_VALIDATION, "bad slot");
   int rc = agb::check_async_status(s);
   if (rc) return rc;
@@ -2157,6 +2169,7 @@ int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap, int64
 int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int beam_width,
                      ag_assignment* out, ag_triple* triples, int32_t triples_cap,
                      int32_t* occupancy) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !q || !engines) return fail(AG_ERR_VALIDATION, "null argument");
   if (beam_width < 1) return fail(AG_ERR_VALIDATION, "beam width < 1");
   const int R = q->n_requests;

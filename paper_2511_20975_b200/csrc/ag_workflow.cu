@@ -157,6 +157,7 @@ using agb::fail;
 
 extern "C" int ag_select_per_workflow_host(ag_ctx* ctx, const ag_truth* th, double tolerance,
                                            uint64_t* chosen, uint64_t* hits_out) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !th || !chosen) return fail(AG_ERR_VALIDATION, "null argument");
   const int R = th->n_requests;
   if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
@@ -210,7 +211,9 @@ extern "C" int ag_select_per_workflow_host(ag_ctx* ctx, const ag_truth* th, doub
   agb::Best b;
   AG_CUDA(cudaMemcpyAsync(&b, final_best, sizeof b, cudaMemcpyDeviceToHost, s));
   AG_CUDA(cudaStreamSynchronize(s));
-  if (b.idx == 0xffffffffu) return fail(AG_ERR_VALIDATION, "per-workflow scan found no configuration");
+  // found <=> a finite static cost: index 0xffffffff is a valid configuration
+  // when M^N == 2^32, so the index cannot double as the not-found sentinel
+  if (!(b.cost < INFINITY)) return fail(AG_ERR_VALIDATION, "per-workflow scan found no configuration");
   *chosen = b.idx;
   if (hits_out) {
     uint32_t h = 0;

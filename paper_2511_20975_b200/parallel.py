@@ -68,7 +68,8 @@ def merge_records(gathered: np.ndarray, rank: int):
 
 
 def all_gather_records(rec: np.ndarray, group=None, device=None) -> np.ndarray:
-    """One all-gather of the per-shard records (NCCL on GPUs, gloo on CPU)."""
+    """One all-gather of host records (gloo on CPU ranks; the host mirror of
+    exchange_records for tests and CPU-only callers)."""
     import torch
     import torch.distributed as dist
 
@@ -83,59 +84,80 @@ def all_gather_records(rec: np.ndarray, group=None, device=None) -> np.ndarray:
     return np.stack([p.cpu().numpy() for p in parts]).view(np.uint64)
 
 
-def route_space_sharded(dev, truth_dev, router, rank, world, load_ctx=None, out=None):
-    """Config 4: every rank enumerates its canonical-index shard of every
-    request, then one all-gather of per-shard records.  Returns the local
-    result, the global counts, this shard's global offsets, and (with a load
-    context) the global runtime-cost choice."""
+def exchange_records(rec, world: int, group=None):
+    """The one collective of the sharded path: all-gather of the [R, 4] int64
+    record tensor into [world, R, 4] (NCCL over NVLink for device tensors,
+    gloo for CPU tensors).  Enqueued on the caller's current stream, no host
+    synchronisation."""
+    import torch
+    import torch.distributed as dist
+
+    if world == 1 or not (dist.is_available() and dist.is_initialized()):
+        return rec.unsqueeze(0)
+    rec = rec.contiguous()
+    out = torch.empty((world * rec.shape[0],) + tuple(rec.shape[1:]), dtype=rec.dtype, device=rec.device)
+    dist.all_gather_into_tensor(out, rec, group=group)
+    return out.view((world,) + tuple(rec.shape))
+
+
+def shard_records(dev, res, n_requests: int, load_ctx=None):
+    """The [R, 4] int64 device records of this shard (ag_shard_records):
+    {count, estimate bits, static-cost bits, index} of the runtime-cost
+    minimum, or counts only without a load context."""
+    import ctypes as C
+
     import torch
 
-    from .scheduler import PER_INPUT_RUNTIME_COST, select_per_input
+    from ._capi import check, lib
+    from .routing import _ptr
+    from .scheduler import PER_INPUT_RUNTIME_COST
 
+    rec = torch.zeros((max(n_requests, 1), REC_WORDS), dtype=torch.int64, device=dev.torch_device)
+    if load_ctx is None:
+        rec[:n_requests, 0] = res.counts[:n_requests].to(torch.int64)
+        return rec[:n_requests]
+    load = load_ctx.c()
+    check(lib().ag_shard_records(dev.handle, C.c_void_p(_ptr(res.indices)), C.c_void_p(_ptr(res.offsets)),
+                                 n_requests, PER_INPUT_RUNTIME_COST, C.byref(load), C.c_void_p(_ptr(rec))))
+    return rec[:n_requests]
+
+
+def merge_device(dev, gathered, rank: int):
+    """ag_merge_records over the gathered [world, R, 4] records: (global
+    counts, this rank's offsets, (best estimate, best static cost, best
+    index)) as device tensors."""
+    import ctypes as C
+
+    import torch
+
+    from ._capi import check, lib
+    from .routing import _ptr
+
+    world, R = int(gathered.shape[0]), int(gathered.shape[1])
+    kw = dict(device=gathered.device)
+    total = torch.empty(max(R, 1), dtype=torch.int64, **kw)
+    before = torch.empty(max(R, 1), dtype=torch.int64, **kw)
+    bi = torch.empty(max(R, 1), dtype=torch.int64, **kw)
+    be = torch.empty(max(R, 1), dtype=torch.float64, **kw)
+    bc = torch.empty(max(R, 1), dtype=torch.float64, **kw)
+    check(lib().ag_merge_records(dev.handle, C.c_void_p(_ptr(gathered)), world, rank, R,
+                                 *[C.c_void_p(_ptr(t)) for t in (total, before, bi, be, bc)]))
+    return total[:R], before[:R], (be[:R], bc[:R], bi[:R])
+
+
+def route_space_sharded(dev, truth_dev, router, rank, world, load_ctx=None, out=None, group=None):
+    """Config 4: every rank enumerates its canonical-index shard of every
+    request (ag_route_enumerate over [begin, end)), reduces it to one 32-byte
+    record per request on the device (ag_shard_records), then ONE all-gather
+    of the records and a device-side merge (ag_merge_records).  No host
+    round trip anywhere: everything is enqueued on the device's stream.
+    Returns the local result, the global counts, this shard's global offsets
+    and the global (estimate, static cost, index) choice, as device tensors
+    (the choice is meaningful only with a load context)."""
     begin, end = shard_range(dev.space.size, rank, world)
     res = dev.route_enumerate(truth_dev, router, begin, end, out=out)
     R = truth_dev.n_requests
-    counts = res.counts.cpu().numpy().astype(np.uint64)
-    if load_ctx is not None:
-        nz = counts > 0
-        ch, est = select_per_input(dev, res.indices, res.offsets, PER_INPUT_RUNTIME_COST, load_ctx) \
-            if nz.all() else _select_nonempty(dev, res, load_ctx, nz)
-        best_i = ch.cpu().numpy().view(np.uint32).astype(np.uint64)
-        best_e = est.cpu().numpy()
-        cost = np.asarray(dev.space.cost)
-        digits = [(best_i // dev.space.m ** (dev.space.n - 1 - a)) % dev.space.m
-                  for a in range(dev.space.n)]
-        best_c = np.zeros(R)
-        for d in digits:  # static_cost: left fold in agent order
-            best_c = best_c + cost[d.astype(np.int64)]
-    else:
-        best_e = np.zeros(R)
-        best_c = np.zeros(R)
-        best_i = np.zeros(R, np.uint64)
-    rec = pack_records(counts, best_e, best_c, best_i)
-    torch.cuda.synchronize()
-    gathered = all_gather_records(rec, device=dev.torch_device)
-    total, before, best = merge_records(gathered, rank)
+    rec = shard_records(dev, res, R, load_ctx)
+    gathered = exchange_records(rec, world, group)
+    total, before, best = merge_device(dev, gathered, rank)
     return res, total, before, best
-
-
-def _select_nonempty(dev, res, load_ctx, nz):
-    """select_per_input over the requests whose shard is non-empty."""
-    import torch
-
-    from .scheduler import PER_INPUT_RUNTIME_COST, select_per_input
-
-    R = len(nz)
-    ch = torch.zeros(R, dtype=torch.int32, device=dev.torch_device)
-    est = torch.full((R,), float("inf"), dtype=torch.float64, device=dev.torch_device)
-    ids = np.nonzero(nz)[0]
-    if len(ids):
-        offs = res.offsets.cpu().numpy()
-        sub_offs = np.concatenate([[0], np.cumsum(offs[ids + 1] - offs[ids])]).astype(np.int64)
-        parts = [res.indices[int(offs[r]):int(offs[r + 1])] for r in ids]
-        mem = torch.cat(parts)
-        c2, e2 = select_per_input(dev, mem, torch.from_numpy(sub_offs).to(dev.torch_device),
-                                  PER_INPUT_RUNTIME_COST, load_ctx)
-        ch[torch.from_numpy(ids).to(dev.torch_device)] = c2
-        est[torch.from_numpy(ids).to(dev.torch_device)] = e2
-    return ch, est

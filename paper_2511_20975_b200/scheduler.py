@@ -213,10 +213,14 @@ class RuntimeCostContext:
         return CLoad(len(self.slots), *[_ptr(a) for a in self._arrs])
 
 
-def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_COST, ctx=None):
+def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_COST, ctx=None,
+                     check_errors=True):
     """select_per_input_config for every request of a member CSR (device
     tensors: members int32 [total], offsets int64 [R+1]).  Returns device
-    tensors (chosen canonical index, estimate)."""
+    tensors (chosen canonical index, estimate).  The C call is asynchronous;
+    with check_errors the stream is synchronised so that the reference's
+    ValidationErrors (an empty set, a tier missing from the load context)
+    raise here, as select_per_input_config throws (workload.cpp:140-156)."""
     import torch
 
     R = offsets.numel() - 1
@@ -226,6 +230,8 @@ def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_CO
     check(lib().ag_select_per_input(device.handle, C.c_void_p(_ptr(members)), C.c_void_p(_ptr(offsets)),
                                     R, kind, C.byref(load) if load is not None else None,
                                     C.c_void_p(_ptr(chosen)), C.c_void_p(_ptr(est))))
+    if check_errors:
+        check(lib().ag_ctx_synchronize(device.handle))
     return chosen[:R], est[:R]
 
 

@@ -63,7 +63,12 @@ def _worker(rank, world, port, q):
                 best_c.append(np.inf)
                 best_i.append(0)
         rec = PL.pack_records(counts, best_e, best_c, best_i)
-        gathered = PL.all_gather_records(rec)
+        # the sharded path's one collective, on CPU tensors over gloo
+        import torch
+        g = PL.exchange_records(torch.from_numpy(rec.view(np.int64).copy()), world)
+        assert tuple(g.shape) == (world, R, PL.REC_WORDS)
+        gathered = g.numpy().view(np.uint64)
+        assert np.array_equal(gathered, PL.all_gather_records(rec))
         total, before, (ge, gc, gi) = PL.merge_records(gathered, rank)
         # the whole-space oracle
         ok = True
@@ -92,3 +97,20 @@ def test_sharded_merge_gloo_world2():
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, True), (1, True)]
+
+
+def test_bench_spawns_one_rank_per_gpu():
+    """`bench.py --gpus N` without a launcher re-executes itself under
+    torchrun (one process per GPU, rendezvous on 127.0.0.1); the ranks join
+    one process group and rank 0 reports n_gpus = N."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--spawn-selftest"],
+                         capture_output=True, text=True, timeout=240, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["ranks_joined"] == 2 and line["launcher"] == "torchrun"
