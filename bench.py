@@ -326,6 +326,8 @@ def run_sched(P, W, dev, args, rounds=None, beam=SCHED_BEAM, exhaustive=False):
 
     _, h, assigned = c3.run(on_round=on_round)
     capi = np.asarray(capi_us)
+    disp = np.asarray(c3.dispatch_us[args.sched_warmup:])
+    both = capi + disp[: len(capi)]
     devt = np.asarray(dev_us)
     free = np.asarray(free)
     by_free = {}
@@ -337,6 +339,9 @@ def run_sched(P, W, dev, args, rounds=None, beam=SCHED_BEAM, exhaustive=False):
             "mean_us": float(capi.mean()),
             "device_p50_us": float(np.percentile(devt, 50)),
             "device_p99_us": float(np.percentile(devt, 99)),
+            "dispatch_p50_us": float(np.percentile(disp, 50)), "dispatch_p99_us": float(np.percentile(disp, 99)),
+            "round_plus_dispatch_p50_us": float(np.percentile(both, 50)),
+            "round_plus_dispatch_p99_us": float(np.percentile(both, 99)),
             "rounds": len(capi), "warmup_rounds": args.sched_warmup, "assigned": int(assigned),
             "by_free_slots": by_free,
             "decision_hash": f"{h:016x}",
@@ -847,6 +852,8 @@ def summarize(line, sched, deep, noisy, linear, chain, config5, select=None, con
                            "dev_p50": _r(sched["device_p50_us"]), "dev_p99": _r(sched["device_p99_us"]),
                            "by_free": {k: [_r(v["p50_us"]), _r(v["p99_us"])]
                                        for k, v in sched["by_free_slots"].items()},
+                           "with_dispatch": [_r(sched["round_plus_dispatch_p50_us"]),
+                                             _r(sched["round_plus_dispatch_p99_us"])],
                            "hash": sched["decision_hash"]}
         for name, v in (sched.get("variants") or {}).items():
             out[f"sched_{name}_us"] = {"p50": _r(v["p50_us"]), "p99": _r(v["p99_us"]),

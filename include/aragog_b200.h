@@ -291,6 +291,9 @@ int ag_beam_schedule(ag_ctx* ctx, const ag_queue* queue,
  * masks); rounds read them in place and dispatch prunes them in place. */
 typedef struct ag_sched ag_sched;
 
+/* max_requests: requests resident at once; max_configs: the viable-list pool
+ * (u32 canonical indices) the resident requests share -- a capacity: when an
+ * add does not fit, the live (pruned) lists are packed on the device first. */
 int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs,
                     ag_sched** out);
 void ag_sched_destroy(ag_sched* s);
@@ -310,6 +313,30 @@ int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width,
 /* Request::mark_dispatched for applied triples (request.cpp:70-86): prefix
  * prune of the viable list in HBM, stage -> in flight. */
 int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied);
+/* apply_assignment(assignment, queue, engines, now, service) (scheduler.cpp:
+ * 421-454): the triples in order; one whose pool has no free slot left
+ * (occupancy + triples applied before it on the pool >= slots, engine.h:47)
+ * is stale and dropped, every other one is applied -- Request::
+ * mark_dispatched, the prefix prune of ag_sched_dispatch.  engines as passed
+ * to the round; applied [n] (optional) receives 1 / 0 per triple. */
+int ag_sched_apply(ag_sched* s, const ag_engines* engines, int32_t n,
+                   const ag_triple* triples, uint8_t* applied, int32_t* n_applied,
+                   int32_t* n_stale);
+/* audit_round_fairness(queue, engines, assignment) (scheduler.cpp:456-480)
+ * against the last round's queue (call it right after ag_sched_round, before
+ * any dispatch / complete / add / remove): an unassigned ready pair whose
+ * allowed engines at its point of the walk are non-empty is a violation.
+ * One kernel over every pair; n <= 2048 triples.  viol_ids / viol_agents
+ * [cap] receive the violations in pair order (RequestId, agent), n_viol
+ * their number. */
+int ag_sched_audit(ag_sched* s, const ag_engines* engines, int32_t n,
+                   const ag_triple* triples, uint64_t* viol_ids, int32_t* viol_agents,
+                   int32_t cap, int32_t* n_viol);
+/* Stateless audit_round_fairness(queue, engines, assignment): the queue as
+ * for ag_beam_schedule, triples' request_index = container index. */
+int ag_audit_round_fairness(ag_ctx* ctx, const ag_queue* queue, const ag_engines* engines,
+                            int32_t n, const ag_triple* triples, uint64_t* viol_ids,
+                            int32_t* viol_agents, int32_t cap, int32_t* n_viol);
 /* diagnostics of the last round, 16 u64: [0..4] device timestamps (ns):
  * start, deltas applied, first candidates published, walk done, finalized;
  * [5..8] walk cycles (find, build, rank, adopt); [9..10] walk steps and
@@ -318,6 +345,9 @@ int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied);
 int ag_sched_round_timing(ag_sched* s, uint64_t* out16);
 /* host wall time (us) of the last ag_sched_round call, entry to return */
 double ag_sched_last_round_us(const ag_sched* s);
+/* the same call split on the host clock (us): record preparation, the launch
+ * call, waiting for the round's completion flag, reading the result back */
+int ag_sched_round_host_timing(const ag_sched* s, double* out4);
 /* read back one request's current viable list (host buffer) */
 int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap,
                     int64_t* n);

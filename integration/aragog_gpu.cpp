@@ -360,9 +360,20 @@ Assignment beam_schedule(const std::vector<const Request*>& queue,
   int max_model = 1;
   for (const EngineState& e : engines) max_model = std::max(max_model, e.model);
   const WorkflowGraph* graph = nullptr;
+  // one GPU context orders every request's ready agents by one graph's
+  // depth / declaration priority (two_level_order, scheduler.cpp:238-242):
+  // distinct graph objects are accepted only when structurally identical
+  auto same_graph = [](const WorkflowGraph& a, const WorkflowGraph& b) {
+    if (a.num_agents() != b.num_agents()) return false;
+    for (int p = 0; p < a.num_agents(); ++p)
+      if (a.declaration_index(p) != b.declaration_index(p) || a.depth(p) != b.depth(p) ||
+          a.successors(p) != b.successors(p))
+        return false;
+    return true;
+  };
   for (const Request* r : queue) {
     if (!graph) graph = r->graph;
-    else if (r->graph != graph && r->graph->num_agents() != graph->num_agents())
+    else if (r->graph != graph && !same_graph(*r->graph, *graph))
       throw ValidationError("GPU scheduler needs one workflow per round");
     for (const Configuration& c : r->viable)
       for (int d : c.models) max_model = std::max(max_model, d);

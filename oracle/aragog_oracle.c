@@ -1053,6 +1053,57 @@ static int score_assignment(const round_ctx* c, const bstate* s, double* util,
   return AGO_OK;
 }
 
+/* audit_round_fairness (scheduler.cpp:456-480): replay the assignment's
+ * triples in pair order (a cursor that advances only on a match) from
+ * initial_state; an unassigned pair with allowed engines is a violation. */
+int ago_audit_round_fairness(const ago_queue* q, const ago_engines* e,
+                             const ago_triple* triples, int n_triples,
+                             uint64_t* viol_ids, int32_t* viol_agents, int cap,
+                             int* n_viol) {
+  round_ctx c;
+  int rc = ctx_build(&c, q, e);
+  if (rc) {
+    ctx_free(&c);
+    return rc;
+  }
+  bstate st;
+  rc = initial_state(&c, &st, n_triples + 1);
+  if (rc) {
+    bs_free(&st);
+    ctx_free(&c);
+    return rc;
+  }
+  int pos = 0, nv = 0;
+  for (int pi = 0; pi < c.n_pairs; ++pi) {
+    int assigned = pos < n_triples && triples[pos].request_index == c.pair_req[pi] &&
+                   triples[pos].agent == c.pair_agent[pi];
+    if (assigned) {
+      int mdl = triples[pos].model;
+      int eng = mdl >= 0 && mdl < c.n_m2e ? c.model_to_engine[mdl] : -1;
+      if (eng < 0) {
+        bs_free(&st);
+        ctx_free(&c);
+        return fail(AGO_VALIDATION, "assignment names a model without an engine pool");
+      }
+      bstate next;
+      extend_state(&c, &st, pi, eng, &next);
+      bs_free(&st);
+      st = next;
+      ++pos;
+    } else if (allowed_engines(&c, &st, pi) != 0) {
+      if (nv < cap) {
+        viol_ids[nv] = q->ids[c.pair_req[pi]];
+        viol_agents[nv] = c.pair_agent[pi];
+      }
+      ++nv;
+    }
+  }
+  *n_viol = nv;
+  bs_free(&st);
+  ctx_free(&c);
+  return AGO_OK;
+}
+
 /* beam_schedule (scheduler.cpp:289-378) */
 int ago_beam_schedule(const ago_queue* q, const ago_engines* e, int width,
                       ago_triple* triples, int triples_cap,

@@ -168,6 +168,13 @@ int ago_beam_schedule(const ago_queue* q, const ago_engines* e, int width,
                       ago_triple* triples, int triples_cap,
                       int32_t* occupancy_out, ago_assignment* out);
 
+/* audit_round_fairness (scheduler.cpp:456-480): violations written as
+ * (RequestId, agent) in pair order, *n_viol their number. */
+int ago_audit_round_fairness(const ago_queue* q, const ago_engines* e,
+                             const ago_triple* triples, int n_triples,
+                             uint64_t* viol_ids, int32_t* viol_agents, int cap,
+                             int* n_viol);
+
 /* Request::mark_dispatched prefix prune (request.cpp:70-86) on one request's
  * list; returns new length (or -1 when nothing survives). */
 int64_t ago_prefix_prune(int n, int m, uint64_t* viable, int64_t len, int agent,

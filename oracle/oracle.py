@@ -324,6 +324,23 @@ def beam_schedule(qd, width):
                 states_explored=out.states_explored)
 
 
+def audit_round_fairness(qd, triples):
+    """audit_round_fairness (scheduler.cpp:456-480): triples as
+    (request_index, request_id, agent, model); returns [(RequestId, agent)]."""
+    q, e = qd.cq(), qd.ce()
+    n = len(triples)
+    tr = (Triple * max(1, n))()
+    for i, (qi, rid, a, mdl) in enumerate(triples):
+        tr[i].request_index, tr[i].request_id, tr[i].agent, tr[i].model = qi, rid, a, mdl
+    cap = max(1, int((qd.stages == READY).sum()))
+    ids = np.zeros(cap, np.uint64)
+    ags = np.zeros(cap, np.int32)
+    nv = C.c_int()
+    _check(_lib().ago_audit_round_fairness(C.byref(q), C.byref(e), tr, n, C.c_void_p(_p(ids)),
+                                           C.c_void_p(_p(ags)), cap, C.byref(nv)))
+    return [(int(ids[i]), int(ags[i])) for i in range(min(nv.value, cap))]
+
+
 def generate_snapshot(seed, index):
     s = Snapshot()
     _check(_lib().ago_generate_snapshot(C.c_uint64(seed), C.c_uint64(index), C.byref(s)))

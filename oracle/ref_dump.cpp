@@ -468,6 +468,39 @@ json dump_rounds() {
         res[std::to_string(w)] = aj;
       }
       j["beam"] = res;
+      // audit_round_fairness of doctored width-4 assignments (the
+      // scheduler_test.cpp:211-229 pattern): dropped, truncated, reordered
+      {
+        Assignment a = beam_schedule(queue, engines, SchedulerParams{4});
+        const std::size_t T = a.triples.size();
+        std::vector<std::vector<AssignmentTriple>> docs;
+        if (T >= 1) {
+          docs.push_back(std::vector<AssignmentTriple>(a.triples.begin() + 1, a.triples.end()));
+          auto mid = a.triples;
+          mid.erase(mid.begin() + (long)(T / 2));
+          docs.push_back(mid);
+        }
+        docs.push_back(std::vector<AssignmentTriple>(a.triples.begin(), a.triples.begin() + (long)(T / 2)));
+        if (T >= 2) {
+          auto sw = a.triples;
+          std::swap(sw[0], sw[1]);
+          docs.push_back(sw);
+        }
+        docs.push_back({});
+        json aud = json::array();
+        for (const auto& d : docs) {
+          Assignment x = a;
+          x.triples = d;
+          json tj = json::array();
+          for (const auto& t : d)
+            tj.push_back({t.request_index, t.request, t.agent, t.model});
+          json vj = json::array();
+          for (const FairnessViolation& v : audit_round_fairness(queue, engines, x))
+            vj.push_back({v.request, v.agent});
+          aud.push_back({{"triples", tj}, {"violations", vj}});
+        }
+        j["audit"] = aud;
+      }
       out.push_back(j);
     }
   }

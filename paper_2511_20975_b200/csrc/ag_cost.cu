@@ -96,47 +96,45 @@ __global__ void __launch_bounds__(256) k_cost_prefix(const __grid_constant__ Cos
 // gets no task.
 __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ CostArgs A) {
   __shared__ int32_t s_wsum[32];
-  __shared__ int32_t s_carry;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  if (tid == 0) s_carry = 0;
   const uint64_t total = A.offsets[A.R] - A.offsets[0];
   const uint64_t tq = (total + kTaskCap - 1) / kTaskCap;
   const uint64_t ts = tq > kTask ? tq : kTask;
   if (tid == 0) *A.tsize = ts;
+  // thread tid plans the contiguous requests [r0, r1): one pass, one scan
+  const int per = (A.R + 1023) / 1024;
+  const int r0 = min(A.R, tid * per), r1 = min(A.R, r0 + per);
+  int32_t mine = 0;
+  for (int r = r0; r < r1; ++r) {
+    const uint64_t len = A.offsets[r + 1] - A.offsets[r];
+    if (len == 0 && !A.allow_empty) atomicOr(A.status, 2);
+    mine += (int32_t)((len + ts - 1) / ts);
+  }
+  int32_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_wsum[w] = x;
   __syncthreads();
-  for (int base = 0; base < A.R; base += 1024) {
-    const int r = base + tid;
-    int32_t nt = 0;
-    if (r < A.R) {
-      const uint64_t len = A.offsets[r + 1] - A.offsets[r];
-      if (len == 0 && !A.allow_empty) atomicOr(A.status, 2);
-      nt = (int32_t)((len + ts - 1) / ts);
-    }
-    int32_t x = nt;
+  if (w == 0) {
+    const int32_t v = s_wsum[lane];
+    int32_t z = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
     }
-    if (lane == 31) s_wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int32_t v = s_wsum[lane], z = v;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int32_t y = __shfl_up_sync(0xffffffffu, z, o);
-        if (lane >= o) z += y;
-      }
-      s_wsum[lane] = z - v;
-    }
-    __syncthreads();
-    const int32_t carry = s_carry;
-    if (r < A.R) A.r_task[r] = carry + s_wsum[w] + x - nt;
-    __syncthreads();
-    if (tid == 1023) s_carry = carry + s_wsum[31] + x;
-    __syncthreads();
+    s_wsum[lane] = z - v;
+    if (lane == 31) A.r_task[A.R] = z;
   }
-  if (tid == 0) A.r_task[A.R] = s_carry;
+  __syncthreads();
+  int32_t acc = s_wsum[w] + x - mine;
+  for (int r = r0; r < r1; ++r) {
+    A.r_task[r] = acc;
+    acc += (int32_t)((A.offsets[r + 1] - A.offsets[r] + ts - 1) / ts);
+  }
 }
 
 // SFX = N - k suffix digits per member (1..4 specialised; 0 = runtime, <= 16:

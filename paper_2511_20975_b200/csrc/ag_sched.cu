@@ -92,8 +92,11 @@ namespace {
 template <int BM>
 struct RoundShape {
   static constexpr int threads = 512;
-  static constexpr int producers = threads / 4 * 3;  // warps 1-3, 5-7, 9-11 (, 13-15)
+  // warps 1-3, 5-7, 9-11, 13-15; the fast walker (BM > 0) gives warp 1 to
+  // its lookahead (candidate records and histogram rows fetched ahead)
+  static constexpr int producers = threads / 4 * 3 - (BM > 0 ? 32 : 0);
 };
+constexpr int kLookahead = 64;  // lookahead ring entries (a power of two)
 constexpr int kMaxRoundThreads = 512;
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
@@ -165,6 +168,8 @@ struct RoundArgs {
   uint32_t* gmask;  // candidates beyond shared memory
   Cand* grec;
   int cand_cap, hist_cap;
+  int rows_alloc;  // ratio / count rows allocated (>= hist_cap, >= the lookahead ring)
+  int la_rows;     // lookahead ring entries (power of two, <= kLookahead; 0: no lookahead)
   int wor_cap;  // 32-candidate windows: the union of their engine masks
   Node* gnodes;
   int max_nodes;
@@ -313,6 +318,133 @@ struct Child {  // a BeamState child in shared memory (wide beams)
 };
 
 // ------------------------------------------------------------ round kernel
+// Applies refresh records {FIFO position, slot, ready mask}: ready[slot],
+// order[pos] and the position's pair record pinfo[pos] = {slot | first ready
+// agent << 26, that agent's candidate-model mask, viable size, ready-agent
+// count}.  Loads are issued kU at a time so latency (PCIe for mapped host
+// memory) is paid once per batch.  prank(agent): priority rank (depth desc,
+// declaration asc, scheduler.cpp:238-242).
+template <typename PRank>
+__device__ __forceinline__ void apply_records(const int4* __restrict__ rec, int n_rec, int first, int stride, int N,
+                                              uint64_t* ready, const uint32_t* cand, const uint32_t* nviable,
+                                              int32_t* order, uint4* pinfo, PRank prank) {
+  constexpr int kU = 4;
+  for (int i0 = first; i0 < n_rec; i0 += stride * kU) {
+    int4 rc[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * stride;
+      rc[u] = i < n_rec ? rec[i] : make_int4(-1, -1, 0, 0);
+    }
+    uint32_t cm[kU], nvv[kU];
+    int best[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pos = rc[u].x, slot = rc[u].y;
+      const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
+      if (slot >= 0) ready[slot] = r;
+      int bst = -1, br = 1 << 30;
+      for (uint64_t b = r; b; b &= b - 1) {
+        const int ag = __ffsll((long long)b) - 1;
+        const int pr = prank(ag);
+        if (pr < br) br = pr, bst = ag;
+      }
+      best[u] = bst;
+      // the union of the ready agents' candidate models (one agent: its mask)
+      uint32_t c = 0;
+      if (pos >= 0 && slot >= 0)
+        for (uint64_t b = r; b; b &= b - 1) c |= cand[(size_t)slot * N + (__ffsll((long long)b) - 1)];
+      cm[u] = c;
+      nvv[u] = pos >= 0 && slot >= 0 ? nviable[slot] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int pos = rc[u].x, slot = rc[u].y;
+      if (pos < 0) continue;
+      const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
+      const uint32_t nr = slot >= 0 ? (uint32_t)__popcll(r) : 0u;
+      order[pos] = slot;
+      pinfo[pos] = make_uint4((uint32_t)(slot >= 0 ? slot : 0) | ((uint32_t)(best[u] & 63) << 26), cm[u], nvv[u], nr);
+    }
+  }
+}
+
+// Viable-pool compaction: the live requests' lists (pruned in place, so only
+// the device knows their lengths) are packed into a fresh pool in slot-list
+// order, and voff is rewritten.  The pool is then a capacity, not a lifetime
+// budget for every request a session ever adds.
+__global__ void __launch_bounds__(1024) k_pool_scan(const int32_t* __restrict__ live, int n_live,
+                                                    const uint32_t* __restrict__ nviable, uint64_t* new_off,
+                                                    uint64_t* total) {
+  __shared__ uint64_t s_w[32];
+  __shared__ uint64_t s_carry;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int base = 0; base < n_live; base += 1024) {
+    const int i = base + tid;
+    const uint64_t len = i < n_live ? nviable[live[i]] : 0;
+    uint64_t x = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      const uint64_t v = s_w[lane];
+      uint64_t z = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += y;
+      }
+      s_w[lane] = z - v;
+    }
+    __syncthreads();
+    const uint64_t carry = s_carry;
+    if (i < n_live) new_off[i] = carry + s_w[w] + x - len;
+    __syncthreads();
+    if (tid == 1023) s_carry = carry + s_w[31] + x;
+    __syncthreads();
+  }
+  if (tid == 0) *total = s_carry;
+}
+
+__global__ void __launch_bounds__(256) k_pool_copy(const int32_t* __restrict__ live, const uint64_t* __restrict__ new_off,
+                                                   const uint32_t* __restrict__ nviable, uint64_t* voff,
+                                                   const uint32_t* __restrict__ src, uint32_t* __restrict__ dst) {
+  const int s = live[blockIdx.x];
+  const uint64_t from = voff[s], to = new_off[blockIdx.x];
+  const uint32_t len = nviable[s];
+  for (uint32_t q = threadIdx.x; q < len; q += 256) dst[to + q] = src[from + q];
+  __syncthreads();
+  if (threadIdx.x == 0) voff[s] = to;
+}
+
+// Large record batches (a FIFO compaction, a big arrival batch) are applied
+// when they happen, by this kernel, instead of inside the next round's
+// decision latency.
+struct RefreshArgs {
+  int N;
+  uint64_t* ready;
+  const uint32_t* cand;
+  const uint32_t* nviable;
+  int32_t* order;
+  uint4* pinfo;
+  int8_t prio_rank[64];
+};
+
+__global__ void __launch_bounds__(256) k_sched_refresh(const int4* __restrict__ rec, int n_rec,
+                                                       const __grid_constant__ RefreshArgs A) {
+  __shared__ int8_t s_pr[64];
+  if (threadIdx.x < 64) s_pr[threadIdx.x] = A.prio_rank[threadIdx.x];
+  __syncthreads();
+  apply_records(rec, n_rec, blockIdx.x * 256 + threadIdx.x, gridDim.x * 256, A.N, A.ready, A.cand, A.nviable,
+                A.order, A.pinfo, [&](int ag) { return (int)s_pr[ag]; });
+}
+
 template <int BM>
 __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(RoundArgs A) {
   constexpr int kRoundThreads = RoundShape<BM>::threads, kProducers = RoundShape<BM>::producers;
@@ -343,17 +475,24 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
   __shared__ double e_weight[kMaxEng];
   __shared__ int8_t e_m2e[32], s_prio[64], s_prank[64];
   __shared__ uint32_t s_emtab[4][256];  // model mask -> engine mask, one byte at a time
+  // lookahead ring (BM > 0): candidate records and engine masks; their count
+  // / ratio rows live in the staging rows below
+  __shared__ __align__(16) Cand s_la_rec[BM > 0 ? kLookahead : 1];
+  __shared__ uint32_t s_la_mask[BM > 0 ? kLookahead : 1];
+  __shared__ int32_t s_la_idx[BM > 0 ? kLookahead : 1];
+  __shared__ unsigned s_la_head, s_la_tail, s_la_done;
+  __shared__ uint32_t s_U;  // the walker's current free-engine union (shrinks)
   // dynamic: nodes | children (wide beams) | ratio rows | cand records | cand masks | count rows
   Node* s_nodes = reinterpret_cast<Node*>(dsm);
   Child* children = reinterpret_cast<Child*>(s_nodes + kSmemNodes);
   double* h_rat = reinterpret_cast<double*>(children + A.max_children);
-  Cand* c_rec = reinterpret_cast<Cand*>(h_rat + (size_t)A.hist_cap * A.M);
+  Cand* c_rec = reinterpret_cast<Cand*>(h_rat + (size_t)A.rows_alloc * A.M);
   uint32_t* c_mask = reinterpret_cast<uint32_t*>(c_rec + A.cand_cap);
   uint32_t* h_cnt = c_mask + A.cand_cap;
   // per window of 32 candidates, the union of their masks: the walker skips
   // a published window whose union misses every free engine without reading
   // its candidates
-  uint32_t* s_wor = h_cnt + (size_t)A.hist_cap * A.M;
+  uint32_t* s_wor = h_cnt + (size_t)A.rows_alloc * A.M;
 
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int N = A.N, M = A.M, B = A.B;
@@ -364,6 +503,11 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
     s_rows = 0;
     s_prod_done = 0;
     s_walk_done = 0;
+    s_la_head = s_la_tail = s_la_done = 0;
+    uint32_t u0 = 0;
+    for (int e = 0; e < A.eng.E; ++e)
+      if (A.eng.slots[e] - A.eng.occ[e] > 0) u0 |= 1u << e;
+    s_U = u0;
     s_carry[0] = s_carry[1] = s_carry[2] = 0;
     if (A.timing) A.timing[0] = gtimer();
     if (*A.async_status) {
@@ -415,40 +559,8 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
           if (i < A.Q) A.cidx[i] = v[u];
         }
       }
-    for (int i0 = 0; i0 < A.n_rec; i0 += kRoundThreads * kU) {
-      int4 rc[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * kRoundThreads + tid;
-        rc[u] = i < A.n_rec ? A.h_rec[i] : make_int4(-1, -1, 0, 0);
-      }
-      uint32_t cm[kU], nvv[kU];
-      int best[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int pos = rc[u].x, slot = rc[u].y;
-        const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
-        if (slot >= 0) A.ready[slot] = r;
-        // first ready agent in (depth desc, declaration asc) order
-        int bst = -1, br = 1 << 30;
-        for (uint64_t b = r; b; b &= b - 1) {
-          const int ag = __ffsll((long long)b) - 1;
-          if (A.prio_rank[ag] < br) br = A.prio_rank[ag], bst = ag;
-        }
-        best[u] = bst;
-        cm[u] = pos >= 0 && bst >= 0 ? A.cand[(size_t)slot * N + bst] : 0u;
-        nvv[u] = pos >= 0 ? A.nviable[slot] : 0u;
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int pos = rc[u].x, slot = rc[u].y;
-        if (pos < 0) continue;
-        const uint64_t r = (uint64_t)(uint32_t)rc[u].z | ((uint64_t)(uint32_t)rc[u].w << 32);
-        A.order[pos] = slot;
-        A.pinfo[pos] = make_uint4((uint32_t)slot | ((uint32_t)(best[u] & 63) << 26), cm[u], nvv[u],
-                                  (uint32_t)__popcll(r));
-      }
-    }
+    apply_records(A.h_rec, A.n_rec, tid, kRoundThreads, N, A.ready, A.cand, A.nviable, A.order, A.pinfo,
+                  [&](int ag) { return (int)A.prio_rank[ag]; });
   }
   __syncthreads();
   if (s_status) {
@@ -469,8 +581,122 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
 
   if (wid != 0) {
     if ((wid & 3) == 0) return;  // the walker's SM sub-partition stays quiet
+    if constexpr (BM > 0) {
+      if (wid == 1) {
+        // ============================================= lookahead (warp 1)
+        // Runs ahead of the walker over the published candidate list: the
+        // next candidates whose engine mask meets the walker's current
+        // free-engine union (a superset of the union when the walker gets
+        // there: it only shrinks) go into a ring with their records and
+        // their histogram rows (surv counts, first-touch ratios surv /
+        // initial): up to 16 windows are scanned per pass and up to 32 hits
+        // fetched together, so the walker's steps read shared memory only.
+        const int LA = A.la_rows;
+        unsigned head = 0, have_l = 0;
+        int jl = 0;
+        bool exhausted = false;
+        while (!exhausted) {
+          // room in the ring (entries below the walker's tail are consumed)
+          unsigned tail = 0;
+          if (lane == 0) {
+            for (;;) {
+              tail = *(volatile unsigned*)&s_la_tail;
+              if (head - tail < (unsigned)LA || *(volatile unsigned*)&s_walk_done) break;
+              __nanosleep(32);
+            }
+          }
+          tail = __shfl_sync(kFull, tail, 0);
+          if (*(volatile unsigned*)&s_walk_done) break;
+          const int want = min(32, LA - (int)(head - tail));
+          const uint32_t U = *(volatile uint32_t*)&s_U;
+          int cnt = 0;
+          for (int scanned = 0; cnt < want && scanned < 16; ++scanned) {
+            if ((unsigned)jl >= have_l) {  // published candidates beyond jl, or the final count
+              unsigned v = 0;
+              if (lane == 0) {
+                for (;;) {
+                  const unsigned done = *(volatile unsigned*)&s_prod_done;
+                  v = *(volatile unsigned*)&s_produced;
+                  // with hits in hand, fetch them rather than wait for more
+                  if (v > (unsigned)jl || done || cnt > 0 || *(volatile unsigned*)&s_walk_done) break;
+                  __nanosleep(32);
+                }
+                v = ld_acquire(&s_produced);
+              }
+              have_l = __shfl_sync(kFull, v, 0);
+              if ((unsigned)jl >= have_l) {
+                if (cnt > 0) break;  // fetch first
+                exhausted = true;
+                break;
+              }
+            }
+            if ((jl & 31) == 0) {  // skip published 32-candidate windows whose union misses U
+              const int w0 = jl >> 5, wl = w0 + lane;
+              const bool pub = (unsigned)(wl + 1) * 32u <= have_l;
+              const unsigned sb = __ballot_sync(kFull, !pub || (s_wor[pub ? wl : 0] & U) != 0u);
+              if (sb == 0u) {
+                jl = (w0 + 32) * 32;
+                continue;
+              }
+              jl = (w0 + __ffs(sb) - 1) * 32;
+              if ((unsigned)jl >= have_l) continue;
+            }
+            const int lim = min((int)have_l, (jl & ~31) + 32);
+            const int idx = jl + lane;
+            const uint32_t mk = idx < lim ? (idx < A.cand_cap ? c_mask[idx] : A.gmask[idx - A.cand_cap]) : 0u;
+            unsigned hit = __ballot_sync(kFull, (mk & U) != 0u);
+            const int nh = __popc(hit);
+            const int take = min(nh, want - cnt);
+            if (take < nh) {  // keep the first `take` hits
+              unsigned h2 = hit;
+              for (int k = 0; k < take; ++k) h2 &= h2 - 1;
+              hit &= ~h2;
+            }
+            if ((hit >> lane) & 1u) {
+              const int sl = (int)((head + (unsigned)(cnt + __popc(hit & ((1u << lane) - 1u)))) & (unsigned)(LA - 1));
+              s_la_idx[sl] = idx;
+              s_la_mask[sl] = mk;
+            }
+            cnt += take;
+            // next unexamined candidate: after the last taken hit, or the window end
+            jl = take < nh ? jl + (32 - __clz(hit)) : lim;
+          }
+          __syncwarp();
+          if (cnt) {
+            // fetch: the records, then the histogram rows (cnt * M loads in flight)
+            if (lane < cnt) {
+              const int sl = (int)((head + (unsigned)lane) & (unsigned)(LA - 1));
+              const int idx = s_la_idx[sl];
+              s_la_rec[sl] = idx < A.cand_cap ? c_rec[idx] : A.grec[idx - A.cand_cap];
+            }
+            __syncwarp();
+            for (int e = lane; e < cnt * M; e += 32) {
+              const int k = e / M, mdl = e - k * M;
+              const int sl = (int)((head + (unsigned)k) & (unsigned)(LA - 1));
+              const Cand r = s_la_rec[sl];
+              const int a = (int)(r.slot_agent >> 26), slt = (int)(r.slot_agent & 0x3ffffffu);
+              const uint32_t sv = __ldg(A.hist + ((size_t)slt * N + a) * M + mdl);
+              h_cnt[sl * M + mdl] = sv;
+              h_rat[sl * M + mdl] = (double)sv / (double)r.nvia;
+            }
+            __syncwarp();
+            if (lane == 0) {
+              __threadfence_block();
+              st_release(&s_la_head, head + (unsigned)cnt);
+            }
+            head += (unsigned)cnt;
+          }
+        }
+        if (lane == 0) {
+          __threadfence_block();
+          st_release(&s_la_done, 1u);
+        }
+        return;
+      }
+    }
     // ================================================= producers
-    const int pt = tid - 32 * (1 + (wid >> 2));  // 0 .. kProducers-1
+    // producer index 0 .. kProducers-1 over the producer warps
+    const int pt = tid - 32 * (1 + (wid >> 2) + (BM > 0 && wid > 1 ? 1 : 0));
     const int pw = pt >> 5;
     // the next chunk's pair records are loaded while this one is processed
     uint4 inf[kPer], nxt[kPer];
@@ -599,7 +825,7 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
       // -- one (candidate, model) entry per thread, loads in parallel.  The
       // first rows of the chunk are published with its records, the rest
       // right after.
-      const int c_lo = s_chunk[0], c_hi = min(s_chunk[1], A.hist_cap);
+      const int c_lo = s_chunk[0], c_hi = BM > 0 ? c_lo : min(s_chunk[1], A.hist_cap);
       const int c_mid = min(c_hi, c_lo + 32);
       auto stage_rows = [&](int from, int to) {
         constexpr int kU = 4;
@@ -1417,6 +1643,232 @@ __global__ void __launch_bounds__(256)
   if (threadIdx.x < M) atomicAdd(out + threadIdx.x, h[threadIdx.x]);
 }
 
+// audit_round_fairness (scheduler.cpp:456-480) of an assignment against the
+// session's last round queue, one block.  The reference walks the pairs in
+// two-level order with a cursor into the triples: a triple counts as assigned
+// only while the triples match pairs in increasing pair order (the matched
+// prefix, length L); at an unassigned pair the state is initial_state
+// extended by the matched triples before it, so its allowed_engines is the
+// pair's candidate engines (or, for a request re-touched earlier in the
+// round, the models at the agent over the viable configurations consistent
+// with its earlier triples) & the free mask after those triples.  A
+// non-empty mask is a violation.
+struct AuditArgs {
+  int N, M, Q, n;
+  const int32_t* order;
+  const uint64_t* ready;
+  const uint32_t* cand;
+  const uint64_t* ids;
+  const uint64_t* voff;
+  const uint32_t* nviable;
+  const uint32_t* pool;
+  const int4* trip;  // {request_index, agent, model, -}
+  int32_t* q_slot;   // scratch [Q]: slot of the q-th request of the queue
+  const int32_t* cidx;  // stateless call: container index per FIFO position (else null)
+  int32_t* c_rank;      // scratch [Q]: queue rank of each container index
+  int8_t prio_rank[64];
+  EngDev eng;
+  uint32_t place[kMaxAgents];
+  uint64_t place_magic[kMaxAgents];
+  uint64_t div_m;
+  uint64_t* out_ids;
+  int32_t* out_agents;
+  int cap;
+  int32_t* out;  // [0] violations, [1] status, [2] matched triples
+};
+
+__device__ __forceinline__ uint32_t digit_a(uint32_t c, int a, const AuditArgs& A) {
+  const uint32_t q = A.place[a] == 1 ? c : (uint32_t)__umul64hi(c, A.place_magic[a]);
+  return q - divm(q, A.div_m) * (uint32_t)A.M;
+}
+
+constexpr int kAuditThreads = 1024, kAuditMaxTrip = 2048;
+
+__global__ void __launch_bounds__(kAuditThreads, 1) k_sched_audit(const __grid_constant__ AuditArgs A) {
+  __shared__ int s_wsum[32];
+  __shared__ int s_carry, s_L, s_status;
+  __shared__ uint32_t s_key[kAuditMaxTrip];  // q << 6 | priority rank of the agent
+  __shared__ uint32_t s_fm[kAuditMaxTrip + 1];
+  __shared__ int s_model[kAuditMaxTrip];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int per = (A.Q + kAuditThreads - 1) / kAuditThreads;
+  const int p0 = tid * per, p1 = min(A.Q, p0 + per);
+  // A: queue index of every FIFO position with a ready stage
+  int nq = 0;
+  for (int p = p0; p < p1; ++p) nq += A.ready[A.order[p]] != 0;
+  auto block_scan = [&](int x, int* total) -> int {  // exclusive
+    int y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, y, o);
+      if (lane >= o) y += t;
+    }
+    if (lane == 31) s_wsum[w] = y;
+    __syncthreads();
+    if (w == 0) {
+      const int v = s_wsum[lane];
+      int z = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, z, o);
+        if (lane >= o) z += t;
+      }
+      s_wsum[lane] = z - v;
+      if (lane == 31) s_carry = z;
+    }
+    __syncthreads();
+    const int r = s_wsum[w] + y - x;
+    *total = s_carry;
+    __syncthreads();
+    return r;
+  };
+  int n_queue = 0;
+  const int q0 = block_scan(nq, &n_queue);
+  if (A.cidx)
+    for (int i = tid; i < A.Q; i += kAuditThreads) A.c_rank[i] = -1;
+  __syncthreads();
+  {
+    int q = q0;
+    for (int p = p0; p < p1; ++p) {
+      const int sl = A.order[p];
+      if (!A.ready[sl]) continue;
+      if (A.cidx) {
+        const int c = A.cidx[p];
+        if (c >= 0 && c < A.Q) A.c_rank[c] = q;
+      }
+      A.q_slot[q++] = sl;
+    }
+  }
+  if (tid == 0) s_status = 0;
+  __syncthreads();
+  // B: the matched prefix of the triples (valid pairs in strictly increasing
+  // pair order) and the free mask after each of its triples
+  const int n = min(A.n, kAuditMaxTrip);
+  int first_bad = n;
+  for (int k = tid; k < n; k += kAuditThreads) {
+    const int4 t = A.trip[k];
+    // the triple's queue rank (container order -> FIFO rank for a stateless call)
+    const int qr = A.cidx ? (t.x >= 0 && t.x < A.Q ? A.c_rank[t.x] : -1) : t.x;
+    bool ok = qr >= 0 && qr < n_queue && t.y >= 0 && t.y < A.N;
+    uint32_t key = 0;
+    if (ok) {
+      ok = (A.ready[A.q_slot[qr]] >> t.y) & 1ull;
+      key = ((uint32_t)qr << 6) | (uint32_t)A.prio_rank[t.y];
+    }
+    s_key[k] = key;
+    s_model[k] = t.z;
+    if (!ok) first_bad = min(first_bad, k);
+  }
+  __syncthreads();
+  for (int k = tid; k < n; k += kAuditThreads)
+    if (k > 0 && s_key[k] <= s_key[k - 1]) first_bad = min(first_bad, k);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first_bad = min(first_bad, __shfl_xor_sync(0xffffffffu, first_bad, o));
+  if (tid == 0) s_L = n;
+  __syncthreads();
+  if (lane == 0) atomicMin(&s_L, first_bad);
+  __syncthreads();
+  const int L = s_L;
+  if (tid == 0) {
+    // initial_state (scheduler.cpp:117-128) and extend_state's free mask
+    int occ[kMaxEng];
+    uint32_t fm = 0;
+    for (int e = 0; e < A.eng.E; ++e) {
+      occ[e] = A.eng.occ[e];
+      if (occ[e] > A.eng.slots[e] || occ[e] < 0) s_status = AG_ERR_VALIDATION + 200;
+      if (occ[e] < A.eng.slots[e]) fm |= 1u << e;
+    }
+    s_fm[0] = fm;
+    for (int k = 0; k < L; ++k) {
+      const int mdl = s_model[k];
+      const int e = mdl >= 0 && mdl < 32 ? A.eng.m2e[mdl] : -1;
+      if (e < 0) {
+        s_status = AG_ERR_VALIDATION + 300;  // a triple names a model without a pool
+        break;
+      }
+      if (++occ[e] >= A.eng.slots[e]) fm &= ~(1u << e);
+      s_fm[k + 1] = fm;
+    }
+  }
+  __syncthreads();
+  if (s_status) {
+    if (tid == 0) A.out[1] = s_status;
+    return;
+  }
+  // C: every pair in order; violations counted per thread, then written in
+  // pair order
+  int nv = 0;
+  bool bad_tier = false;
+  for (int pass = 0; pass < 2; ++pass) {
+    int wbase = 0;
+    if (pass == 1) {
+      int tot = 0;
+      wbase = block_scan(nv, &tot);
+      if (tid == 0) A.out[0] = tot;
+    }
+    int q = q0, o = wbase;
+    for (int p = p0; p < p1; ++p) {
+      const int sl = A.order[p];
+      const uint64_t r = A.ready[sl];
+      if (!r) continue;
+      // ready agents in (depth desc, declaration asc) order = by priority rank
+      uint64_t left = r;
+      while (left) {
+        int a = -1, br = 1 << 30;
+        for (uint64_t b = left; b; b &= b - 1) {
+          const int ag = __ffsll((long long)b) - 1;
+          if (A.prio_rank[ag] < br) br = A.prio_rank[ag], a = ag;
+        }
+        left &= ~(1ull << a);
+        const uint32_t key = ((uint32_t)q << 6) | (uint32_t)br;
+        int lo = 0, hi = L;  // lower_bound of key in the matched prefix
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (s_key[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        if (lo < L && s_key[lo] == key) continue;  // assigned
+        const uint32_t cm = A.cand[(size_t)sl * A.N + a];
+        bad_tier |= (cm & ~A.eng.mapped) != 0u;
+        uint32_t models = cm;
+        if (lo > 0 && (s_key[lo - 1] >> 6) == (uint32_t)q) {
+          // re-touched request: models at agent a over the viable
+          // configurations consistent with its earlier triples this round
+          int k0 = lo;
+          while (k0 > 0 && (s_key[k0 - 1] >> 6) == (uint32_t)q) --k0;
+          models = 0;
+          const uint32_t* vl = A.pool + A.voff[sl];
+          for (uint32_t j = 0; j < A.nviable[sl]; ++j) {
+            const uint32_t c = vl[j];
+            bool okc = true;
+            for (int k = k0; k < lo && okc; ++k)
+              okc = (int)digit_a(c, A.trip[k].y, A) == s_model[k];
+            if (okc) models |= 1u << digit_a(c, a, A);
+          }
+        }
+        uint32_t em = 0;
+        for (uint32_t b = models; b; b &= b - 1) {
+          const int e = A.eng.m2e[__ffs(b) - 1];
+          if (e >= 0) em |= 1u << e;
+        }
+        if (em & s_fm[lo]) {
+          if (pass == 0) {
+            ++nv;
+          } else {
+            if (o < A.cap) {
+              A.out_ids[o] = A.ids[sl];
+              A.out_agents[o] = a;
+            }
+            ++o;
+          }
+        }
+      }
+      ++q;
+    }
+  }
+  if (__syncthreads_or(bad_tier) && tid == 0) A.out[1] = AG_ERR_VALIDATION + 100;
+  if (tid == 0) A.out[2] = L;
+}
+
 }  // namespace
 }  // namespace agb
 
@@ -1453,6 +1905,10 @@ struct ag_sched {
   int walker = 0;  // AG_SCHED_WALKER: 0 automatic, 1 always the general walker
   uint32_t round_seq = 0;
   double last_round_us = 0.0;
+  double host_us[4] = {0, 0, 0, 0};  // last round: prep, launch call, wait, readback (host clock)
+  // session changes since creation; the audit needs the last round's queue
+  uint64_t epoch = 1, round_epoch = 0;
+  agb::Scratch d_audit;
   // device
   agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx, d_pinfo;
   agb::Scratch d_cpos, d_det, d_nodes, d_status, d_gam, d_qa, d_upd;  // d_cpos / d_det: candidate overflow
@@ -1472,11 +1928,19 @@ struct ag_sched {
   size_t h_vstage_bytes = 0;
   void* h_ostage = nullptr;  // FIFO re-uploads after a compaction
   size_t h_ostage_bytes = 0;
+  void* h_fstage = nullptr;  // eager refresh records (refresh_records)
+  size_t h_fstage_bytes = 0;
+  cudaEvent_t fstage_free = nullptr;  // the last copy out of h_fstage
+  agb::Scratch d_frec;
+  agb::Scratch d_pool2, d_pscan;  // pool compaction: the other pool, live slots + offsets
+  size_t dev_q = 0;               // positions holding records on the device
   ~ag_sched() {
     if (h_res) cudaFreeHost(h_res);
     if (h_stage) cudaFreeHost(h_stage);
     if (h_rstage) cudaFreeHost(h_rstage);
     if (h_ostage) cudaFreeHost(h_ostage);
+    if (h_fstage) cudaFreeHost(h_fstage);
+    if (fstage_free) cudaEventDestroy(fstage_free);
     if (h_vstage) cudaFreeHost(h_vstage);
   }
 };
@@ -1641,6 +2105,133 @@ int engines_dev(const ag_engines* e, EngDev* out, bool* ordered = nullptr) {
   return AG_OK;
 }
 
+// Packs the live requests' viable lists into the other pool buffer.
+int compact_pool(ag_sched* s) {
+  ag_ctx* ctx = s->ctx;
+  std::vector<int32_t> live;
+  for (int i = 0; i < s->cap; ++i)
+    if (s->live[i]) live.push_back(i);
+  int rc;
+  const size_t nl = live.size();
+  if ((rc = s->d_pool2.ensure(s->pool_cap * 4)) || (rc = s->d_pscan.ensure(4 * nl + 8 * nl + 64))) return rc;
+  char* d = (char*)s->d_pscan.p;
+  int32_t* d_live = (int32_t*)d;
+  uint64_t* d_off = (uint64_t*)(d + ((4 * nl + 15) & ~(size_t)15));
+  uint64_t* d_tot = d_off + nl;
+  uint64_t total = 0;
+  if (nl) {
+    AG_CUDA(cudaMemcpyAsync(d_live, live.data(), 4 * nl, cudaMemcpyHostToDevice, ctx->stream));
+    {
+      Launch L(ctx, K_SCHED_APPLY);
+      k_pool_scan<<<1, 1024, 0, ctx->stream>>>(d_live, (int)nl, (const uint32_t*)s->d_nv.p, d_off, d_tot);
+    }
+    {
+      Launch L(ctx, K_SCHED_APPLY);
+      k_pool_copy<<<(unsigned)nl, 256, 0, ctx->stream>>>(d_live, d_off, (const uint32_t*)s->d_nv.p,
+                                                         (uint64_t*)s->d_voff.p, (const uint32_t*)s->d_pool.p,
+                                                         (uint32_t*)s->d_pool2.p);
+    }
+    AG_CUDA(cudaGetLastError());
+    AG_CUDA(cudaMemcpyAsync(&total, d_tot, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  AG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::swap(s->d_pool.p, s->d_pool2.p);
+  std::swap(s->d_pool.bytes, s->d_pool2.bytes);
+  s->pool_top = total;
+  return AG_OK;
+}
+
+// Pending ready updates, deduplicated (the last one per slot wins).
+void dedup_updates(ag_sched* s) {
+  if (s->upd_slot.size() <= 1) return;
+  if (s->seen.size() != (size_t)s->cap) s->seen.assign(s->cap, 0);
+  const uint32_t stamp = ++s->seen_stamp;
+  size_t w = s->upd_slot.size();
+  for (size_t i = s->upd_slot.size(); i-- > 0;) {
+    const int slot = s->upd_slot[i];
+    if (s->seen[slot] == stamp) continue;
+    s->seen[slot] = stamp;
+    --w;
+    s->upd_slot[w] = slot;
+    s->upd_mask[w] = s->upd_mask[i];
+  }
+  s->upd_slot.erase(s->upd_slot.begin(), s->upd_slot.begin() + w);
+  s->upd_mask.erase(s->upd_mask.begin(), s->upd_mask.begin() + w);
+}
+
+// Refresh records the next round would apply: every FIFO position from the
+// first stale one, then the other slots whose ready mask changed.
+size_t build_records(ag_sched* s, int32_t* r) {
+  const size_t Q = s->order.size();
+  const size_t from = std::min(std::min(s->dirty_from, s->pinfo_from), Q);
+  size_t n = 0;
+  auto put = [&](int32_t pos, int32_t slot) {
+    const uint64_t m = s->ready[slot];
+    if (r) {
+      r[0] = pos, r[1] = slot, r[2] = (int32_t)(uint32_t)m, r[3] = (int32_t)(uint32_t)(m >> 32);
+      r += 4;
+    }
+    ++n;
+  };
+  for (size_t p = from; p < Q; ++p) put((int32_t)p, s->order[p]);
+  for (size_t i = 0; i < s->upd_slot.size(); ++i) {
+    const int32_t p = s->pos_of[s->upd_slot[i]];
+    if (!(p >= 0 && (size_t)p >= from)) put(p, s->upd_slot[i]);
+  }
+  // positions a compaction left behind Q: empty records (their bits clear)
+  for (size_t p = Q; p < s->dev_q; ++p) {
+    if (r) {
+      r[0] = (int32_t)p, r[1] = -1, r[2] = 0, r[3] = 0;
+      r += 4;
+    }
+    ++n;
+  }
+  if (r) s->dev_q = Q;
+  return n;
+}
+
+// Applies large pending record batches now (FIFO compaction, arrival
+// batches), asynchronously on the stream, so the next round's decision only
+// carries the small per-round deltas.
+constexpr size_t kEagerRecords = 256;
+
+int refresh_records(ag_sched* s, bool force) {
+  const size_t Q = s->order.size();
+  const size_t from = std::min(std::min(s->dirty_from, s->pinfo_from), Q);
+  if (!force && (Q - from) + s->upd_slot.size() + (s->dev_q > Q ? s->dev_q - Q : 0) <= kEagerRecords) return AG_OK;
+  dedup_updates(s);
+  const size_t n = build_records(s, nullptr);
+  if (n == 0) return AG_OK;
+  ag_ctx* ctx = s->ctx;
+  int rc;
+  if (!s->fstage_free) AG_CUDA(cudaEventCreateWithFlags(&s->fstage_free, cudaEventDisableTiming));
+  AG_CUDA(cudaEventSynchronize(s->fstage_free));  // h_fstage's previous copy is done
+  if ((rc = ensure_pinned(&s->h_fstage, &s->h_fstage_bytes, n * 16)) || (rc = s->d_frec.ensure(n * 16))) return rc;
+  build_records(s, (int32_t*)s->h_fstage);
+  AG_CUDA(cudaMemcpyAsync(s->d_frec.p, s->h_fstage, n * 16, cudaMemcpyHostToDevice, ctx->stream));
+  AG_CUDA(cudaEventRecord(s->fstage_free, ctx->stream));
+  RefreshArgs A;
+  A.N = s->N;
+  A.ready = (uint64_t*)s->d_ready.p;
+  A.cand = (const uint32_t*)s->d_cand.p;
+  A.nviable = (const uint32_t*)s->d_nv.p;
+  A.order = (int32_t*)s->d_order.p;
+  A.pinfo = (uint4*)s->d_pinfo.p;
+  for (int i = 0; i < 64; ++i) A.prio_rank[i] = 0;
+  for (int t = 0; t < s->N; ++t) A.prio_rank[(int)s->prio[t]] = (int8_t)t;
+  {
+    Launch L(ctx, K_SCHED_PREP);
+    const unsigned blocks = (unsigned)std::min<size_t>(148, (n + 255) / 256);
+    k_sched_refresh<<<blocks, 256, 0, ctx->stream>>>((const int4*)s->d_frec.p, (int)n, A);
+  }
+  AG_CUDA(cudaGetLastError());
+  s->dirty_from = Q;
+  s->pinfo_from = Q;
+  s->upd_slot.clear();
+  s->upd_mask.clear();
+  return AG_OK;
+}
+
 // One round over the session queue (or an explicit FIFO/container mapping).
 constexpr size_t kMappedMax = 32 * 1024;  // round deltas read over PCIe by the kernel
 
@@ -1666,30 +2257,12 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   const size_t max_pairs = (size_t)Q * (size_t)s->N + 1;
   const int max_nodes = (int)std::min<size_t>((size_t)B * max_pairs + 16, (size_t)1 << 30);
   // ---- ready updates (deduplicated: the last one per slot wins)
-  if (s->upd_slot.size() > 1) {
-    if (s->seen.size() != (size_t)s->cap) s->seen.assign(s->cap, 0);
-    const uint32_t stamp = ++s->seen_stamp;
-    size_t w = s->upd_slot.size();
-    for (size_t i = s->upd_slot.size(); i-- > 0;) {
-      const int slot = s->upd_slot[i];
-      if (s->seen[slot] == stamp) continue;
-      s->seen[slot] = stamp;
-      --w;
-      s->upd_slot[w] = slot;
-      s->upd_mask[w] = s->upd_mask[i];
-    }
-    s->upd_slot.erase(s->upd_slot.begin(), s->upd_slot.begin() + w);
-    s->upd_mask.erase(s->upd_mask.begin(), s->upd_mask.begin() + w);
-  }
+  dedup_updates(s);
   const size_t nu = s->upd_slot.size();
   // refresh records: every FIFO position from the first stale one, then the
   // other slots whose ready mask changed (the host mirror holds the masks)
-  const size_t from = std::min(std::min(s->dirty_from, s->pinfo_from), (size_t)Q);
-  size_t n_rec = (size_t)Q - from;
-  for (size_t i = 0; i < nu; ++i) {
-    const int32_t p = s->pos_of[s->upd_slot[i]];
-    n_rec += !(p >= 0 && (size_t)p >= from);
-  }
+  (void)nu;
+  const size_t n_rec = build_records(s, nullptr);
   const size_t off_cidx = n_rec * 16;
   const size_t up_bytes = off_cidx + (cidx_host ? (size_t)Q * 4 : 0) + 16;
   const size_t res_bytes = kOutHeader + sizeof(ag_assignment) + 4 * kMaxEng + (size_t)cap_t * sizeof(ag_triple);
@@ -1699,19 +2272,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
     return rc;
   // the previous round synchronised after its last use of h_rstage / h_res
   char* h = (char*)s->h_rstage;
-  {
-    int32_t* r = reinterpret_cast<int32_t*>(h);
-    auto put = [&](int32_t pos, int32_t slot) {
-      const uint64_t m = s->ready[slot];
-      r[0] = pos, r[1] = slot, r[2] = (int32_t)(uint32_t)m, r[3] = (int32_t)(uint32_t)(m >> 32);
-      r += 4;
-    };
-    for (size_t p = from; p < (size_t)Q; ++p) put((int32_t)p, s->order[p]);
-    for (size_t i = 0; i < nu; ++i) {
-      const int32_t p = s->pos_of[s->upd_slot[i]];
-      if (!(p >= 0 && (size_t)p >= from)) put(p, s->upd_slot[i]);
-    }
-  }
+  build_records(s, reinterpret_cast<int32_t*>(h));
   if (cidx_host) std::memcpy(h + off_cidx, cidx_host, (size_t)Q * 4);
   if (s->h_rstage != s->h_rstage_mapped) {
     if ((rc = dev_ptr(s->h_rstage, &s->h_rstage_dev))) return rc;
@@ -1732,7 +2293,8 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   // ---- shared memory plan: nodes | children | ratio rows | cand records |
   // cand masks | count rows
   const size_t static_bytes = sizeof(int) * 2 * kMaxBeam * kMaxEng + 2 * 8 * kMaxBeam * kMaxBeam +
-                              sizeof(RankKey) * 32 + kMaxBeam * 32 * 4 + 4 * 1024 + 4096;
+                              sizeof(RankKey) * 32 + kMaxBeam * 32 * 4 + 4 * 1024 + 4096 +
+                              kLookahead * (sizeof(Cand) + 8) + 64;
   const size_t max_dyn = 227 * 1024 - static_bytes;
   const size_t fixed = sizeof(Node) * kSmemNodes + sizeof(Child) * (size_t)max_children;
   if (fixed > max_dyn) return fail(AG_ERR_VALIDATION, "beam too wide for one CTA");
@@ -1742,12 +2304,15 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   // the walk visits the head of the candidate list (engines fill quickly):
   // histogram rows and ratios are staged for that head only
   const size_t row_bytes = (size_t)s->M * (sizeof(double) + sizeof(uint32_t));
-  int hist_cap = (int)std::min<size_t>(std::min<size_t>(max_pairs, 512), (48 * 1024) / row_bytes);
+  int hist_cap = bm ? 0 : (int)std::min<size_t>(std::min<size_t>(max_pairs, 512), (48 * 1024) / row_bytes);
   hist_cap &= ~1;  // keeps the records after the ratio rows 16-byte aligned
-  room -= (size_t)hist_cap * row_bytes;
+  // the fast walker's lookahead ring holds its rows in the same area
+  const int la_rows = bm ? kLookahead : 0;
+  const int rows_alloc = std::max(hist_cap, la_rows);
+  room -= (size_t)rows_alloc * row_bytes;
   const int cand_cap = (int)std::min<size_t>(max_pairs, room / (sizeof(Cand) + 4) & ~(size_t)3);
   hist_cap = std::min(hist_cap, cand_cap & ~1);
-  const size_t dyn = fixed + (size_t)hist_cap * row_bytes + (size_t)cand_cap * (sizeof(Cand) + 4) +
+  const size_t dyn = fixed + (size_t)rows_alloc * row_bytes + (size_t)cand_cap * (sizeof(Cand) + 4) +
                      4 * (size_t)wor_cap;
   const size_t g_over = max_pairs > (size_t)cand_cap ? max_pairs - cand_cap : 1;
   if ((rc = s->d_cpos.ensure(g_over * 4)) || (rc = s->d_det.ensure(g_over * sizeof(Cand))) ||
@@ -1791,6 +2356,8 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.cand_cap = cand_cap;
   A.wor_cap = wor_cap;
   A.hist_cap = hist_cap;
+  A.rows_alloc = rows_alloc;
+  A.la_rows = la_rows;
   A.gnodes = (Node*)s->d_nodes.p;
   A.max_nodes = max_nodes;
   A.max_children = max_children;
@@ -1803,6 +2370,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.triples_cap = cap_t;
   A.timing = (unsigned long long*)((char*)s->d_status.p + 32);
   A.async_status = (int32_t*)s->d_status.p;
+  const auto t_prep = std::chrono::steady_clock::now();
   {
     Launch L(ctx, K_SCHED_ROUND);
     if (bm == 1) k_sched_round<1><<<1, RoundShape<1>::threads, dyn, ctx->stream>>>(A);
@@ -1810,6 +2378,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
     else k_sched_round<0><<<1, RoundShape<0>::threads, dyn, ctx->stream>>>(A);
   }
   AG_CUDA(cudaGetLastError());
+  const auto t_launch = std::chrono::steady_clock::now();
   {
     // spin on the round's sequence number in the mapped result header (a
     // stream synchronisation costs several microseconds more); a kernel that
@@ -1819,6 +2388,7 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
       if ((it & 1023u) == 0 && cudaStreamQuery(ctx->stream) != cudaErrorNotReady) break;
     if (*flag != (int32_t)A.seq) AG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  const auto t_seen = std::chrono::steady_clock::now();
   s->dirty_from = Q;
   s->pinfo_from = Q;
   s->upd_slot.clear();
@@ -1842,8 +2412,16 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   if (occupancy) std::memcpy(occupancy, occ, 4 * (size_t)engines->n_engines);
   if (res.n_triples)
     std::memcpy(triples, occ + 4 * kMaxEng, sizeof(ag_triple) * (size_t)res.n_triples);
-  s->last_round_us =
-      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
+  const auto t_end = std::chrono::steady_clock::now();
+  auto us = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::micro>(b - a).count();
+  };
+  s->host_us[0] = us(t_start, t_prep);
+  s->host_us[1] = us(t_prep, t_launch);
+  s->host_us[2] = us(t_launch, t_seen);
+  s->host_us[3] = us(t_seen, t_end);
+  s->last_round_us = us(t_start, t_end);
+  s->round_epoch = s->epoch;
   return AG_OK;
 }
 
@@ -1934,6 +2512,7 @@ int ag_sched_create(ag_ctx* ctx, int32_t max_requests, uint64_t max_configs, ag_
     delete s;
     return rc;
   }
+  cudaMemsetAsync(s->d_pinfo.p, 0, ((size_t)2 * max_requests + 1024) * 16, ctx->stream);
   cudaMemsetAsync(s->d_ready.p, 0, R * 8, ctx->stream);
   cudaMemsetAsync(s->d_status.p, 0, 128, ctx->stream);
   *out = s;
@@ -1947,6 +2526,7 @@ void ag_sched_destroy(ag_sched* s) {
 
 int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
   agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (s) ++s->epoch;
   if (!s || !q) return fail(AG_ERR_VALIDATION, "null argument");
   ag_ctx* ctx = s->ctx;
   const int R = q->n_requests;
@@ -1954,6 +2534,11 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
   if ((int)s->free_slots.size() < R && !s->quarantine.empty()) agb::compact_order(s);
   if ((int)s->free_slots.size() < R) return fail(AG_ERR_VALIDATION, "session is full");
   const uint64_t total = (uint64_t)(q->viable_ptr[R] - q->viable_ptr[0]);
+  if (s->pool_top + total > s->pool_cap) {
+    // removed requests left dead space behind pool_top: pack the live lists
+    int rc0 = agb::compact_pool(s);
+    if (rc0) return rc0;
+  }
   if (s->pool_top + total > s->pool_cap) return fail(AG_ERR_VALIDATION, "session viable pool is full");
   const int N = s->N;
   // Request::make (request.cpp:24-50)
@@ -2013,12 +2598,14 @@ int ag_sched_add(ag_sched* s, const ag_queue* q, int32_t* slots_out) {
     s->pinfo_from = std::min(s->pinfo_from, pos);
   }
   // the viable copy must land before the histogram pass reads it (same stream)
-  const int rc = agb::launch_prune(s, slots, g_begin, {}, &meta);
-  return rc ? rc : agb::flush_order(s);
+  int rc = agb::launch_prune(s, slots, g_begin, {}, &meta);
+  if (rc || (rc = agb::flush_order(s))) return rc;
+  return agb::refresh_records(s, false);
 }
 
 int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
   agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (s) ++s->epoch;
   if (!s) return fail(AG_ERR_VALIDATION, "null argument");
   for (int i = 0; i < n; ++i) {
     const int slot = slots[i];
@@ -2035,11 +2622,13 @@ int ag_sched_remove(ag_sched* s, int32_t n, const int32_t* slots) {
     agb::compact_order(s);
     s->pool_top = 0;  // everything left: reuse the pool
   }
-  return agb::flush_order(s);
+  int rc = agb::flush_order(s);
+  return rc ? rc : agb::refresh_records(s, false);
 }
 
 int ag_sched_complete(ag_sched* s, int32_t slot, int32_t agent) {
   agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (s) ++s->epoch;
   if (!s || slot < 0 || slot >= s->cap || !s->live[slot]) return fail(AG_ERR_VALIDATION, "bad slot");
   const int N = s->N;
   if (agent < 0 || agent >= N || s->stages[(size_t)slot * N + agent] != AG_STAGE_INFLIGHT)
@@ -2069,6 +2658,7 @@ int ag_sched_round(ag_sched* s, const ag_engines* engines, int beam_width, ag_as
 
 int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
   agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (s) ++s->epoch;
   if (!s) return fail(AG_ERR_VALIDATION, "null argument");
   const int N = s->N;
   for (int i = 0; i < n; ++i) {
@@ -2098,6 +2688,127 @@ int ag_sched_dispatch(ag_sched* s, int32_t n, const ag_triple* applied) {
     agb::set_ready(s, slot, agb::ready_of(s, slot));
   }
   return agb::launch_prune(s, g_slot, g_begin, g_am, nullptr);
+}
+
+// apply_assignment (scheduler.cpp:421-454): triples in order; a triple whose
+// engine pool has no free slot left (occupancy + triples applied before it
+// on the same pool >= slots) is stale and dropped, the rest are applied:
+// Request::mark_dispatched (prefix prune on the device, ag_sched_dispatch).
+int ag_sched_apply(ag_sched* s, const ag_engines* engines, int32_t n, const ag_triple* triples,
+                   uint8_t* applied, int32_t* n_applied, int32_t* n_stale) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (!s || !engines || (n > 0 && !triples)) return fail(AG_ERR_VALIDATION, "null argument");
+  std::vector<int> left(std::max(engines->n_engines, 1));
+  std::vector<int> pool_of(64, -1);
+  for (int i = 0; i < engines->n_engines; ++i) {
+    const int mdl = engines->model[i];
+    if (mdl >= 0 && mdl < 64) pool_of[mdl] = i;
+    left[i] = engines->slots[i] - engines->occupancy[i];
+  }
+  std::vector<ag_triple> keep;
+  keep.reserve(n);
+  int na = 0, ns = 0;
+  for (int k = 0; k < n; ++k) {
+    const int mdl = triples[k].model;
+    if (mdl < 0 || mdl >= 64 || pool_of[mdl] < 0)
+      return fail(AG_ERR_VALIDATION, "assignment names a model without an engine pool");
+    const bool ok = left[pool_of[mdl]] > 0;  // EngineState::slots_available (engine.h:47)
+    if (ok) {
+      --left[pool_of[mdl]];
+      keep.push_back(triples[k]);
+      ++na;
+    } else {
+      ++ns;
+    }
+    if (applied) applied[k] = ok ? 1 : 0;
+  }
+  if (n_applied) *n_applied = na;
+  if (n_stale) *n_stale = ns;
+  return keep.empty() ? AG_OK : ag_sched_dispatch(s, (int32_t)keep.size(), keep.data());
+}
+
+namespace agb {
+namespace {
+// the audit kernel over the session's device queue; cidx: container index per
+// FIFO position (device) for a stateless queue, else null
+int audit_impl(ag_sched* s, const ag_engines* engines, int32_t n, const ag_triple* triples, const int32_t* cidx,
+               uint64_t* viol_ids, int32_t* viol_agents, int32_t cap, int32_t* n_viol) {
+  if (n > agb::kAuditMaxTrip) return fail(AG_ERR_VALIDATION, "audit supports at most 2048 triples");
+  agb::EngDev ed;
+  int rc = agb::engines_dev(engines, &ed);
+  if (rc) return rc;
+  ag_ctx* ctx = s->ctx;
+  cudaStream_t st = ctx->stream;
+  const int Q = (int)s->order.size();
+  const size_t tb = 16 * (size_t)std::max(n, 1), qb = 4 * (size_t)std::max(Q, 1);
+  const size_t ob = 16 + 12 * (size_t)std::max(cap, 0);
+  if ((rc = s->d_audit.ensure(tb + 2 * qb + ob + 64)) ||
+      (rc = agb::ensure_pinned(&s->h_stage, &s->h_stage_bytes, tb + ob + 64)))
+    return rc;
+  AG_CUDA(cudaStreamSynchronize(st));  // the staging buffer's previous use
+  int4* ht = (int4*)s->h_stage;
+  for (int k = 0; k < n; ++k) ht[k] = make_int4(triples[k].request_index, triples[k].agent, triples[k].model, 0);
+  char* d = (char*)s->d_audit.p;
+  agb::AuditArgs A;
+  std::memset(&A, 0, sizeof A);
+  A.N = s->N;
+  A.M = s->M;
+  A.Q = Q;
+  A.n = n;
+  A.order = (const int32_t*)s->d_order.p;
+  A.ready = (const uint64_t*)s->d_ready.p;
+  A.cand = (const uint32_t*)s->d_cand.p;
+  A.ids = (const uint64_t*)s->d_ids.p;
+  A.voff = (const uint64_t*)s->d_voff.p;
+  A.nviable = (const uint32_t*)s->d_nv.p;
+  A.pool = (const uint32_t*)s->d_pool.p;
+  A.trip = (const int4*)d;
+  A.q_slot = (int32_t*)(d + tb);
+  for (int t = 0; t < s->N; ++t) A.prio_rank[(int)s->prio[t]] = (int8_t)t;
+  A.eng = ed;
+  std::memcpy(A.place, s->place, sizeof A.place);
+  std::memcpy(A.place_magic, s->place_magic, sizeof A.place_magic);
+  A.div_m = ctx->space->dev().div_m;
+  A.cidx = cidx;
+  A.c_rank = (int32_t*)(d + tb + qb);
+  A.out = (int32_t*)(d + tb + 2 * qb);
+  A.out_ids = (uint64_t*)(d + tb + 2 * qb + 16);
+  A.out_agents = (int32_t*)(d + tb + 2 * qb + 16 + 8 * (size_t)std::max(cap, 0));
+  A.cap = std::max(cap, 0);
+  if (n) AG_CUDA(cudaMemcpyAsync(d, ht, 16 * (size_t)n, cudaMemcpyHostToDevice, st));
+  AG_CUDA(cudaMemsetAsync(A.out, 0, 16, st));
+  {
+    agb::Launch L(ctx, agb::K_SCHED_PREP);
+    agb::k_sched_audit<<<1, agb::kAuditThreads, 0, st>>>(A);
+  }
+  AG_CUDA(cudaGetLastError());
+  char* ho = (char*)s->h_stage + tb;
+  AG_CUDA(cudaMemcpyAsync(ho, A.out, ob, cudaMemcpyDeviceToHost, st));
+  AG_CUDA(cudaStreamSynchronize(st));
+  const int32_t* hout = (const int32_t*)ho;
+  if (hout[1] == AG_ERR_VALIDATION + 100) return fail(AG_ERR_VALIDATION, "viable model tier without an engine pool");
+  if (hout[1] == AG_ERR_VALIDATION + 200) return fail(AG_ERR_VALIDATION, "engine over capacity");
+  if (hout[1] == AG_ERR_VALIDATION + 300)
+    return fail(AG_ERR_VALIDATION, "assignment names a model without an engine pool");
+  if (hout[1]) return fail(AG_ERR_INTERNAL, "audit failed");
+  *n_viol = hout[0];
+  const int k = std::min(hout[0], std::max(cap, 0));
+  if (k && viol_ids) std::memcpy(viol_ids, ho + 16, 8 * (size_t)k);
+  if (k && viol_agents) std::memcpy(viol_agents, ho + 16 + 8 * (size_t)std::max(cap, 0), 4 * (size_t)k);
+  return AG_OK;
+}
+}  // namespace
+}  // namespace agb
+
+// audit_round_fairness (scheduler.cpp:456-480) over the last round's queue:
+// must follow ag_sched_round with no session change in between.
+int ag_sched_audit(ag_sched* s, const ag_engines* engines, int32_t n, const ag_triple* triples,
+                   uint64_t* viol_ids, int32_t* viol_agents, int32_t cap, int32_t* n_viol) {
+  agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
+  if (!s || !engines || !n_viol || (n > 0 && !triples)) return fail(AG_ERR_VALIDATION, "null argument");
+  if (s->round_epoch != s->epoch)
+    return fail(AG_ERR_VALIDATION, "audit needs the queue of the last round (session changed since)");
+  return agb::audit_impl(s, engines, n, triples, nullptr, viol_ids, viol_agents, cap, n_viol);
 }
 
 int ag_sched_queued_ahead(ag_sched* s, int32_t* out) {
@@ -2145,6 +2856,12 @@ int ag_sched_round_timing(ag_sched* s, uint64_t* ns) {
 
 double ag_sched_last_round_us(const ag_sched* s) { return s ? s->last_round_us : 0.0; }
 
+int ag_sched_round_host_timing(const ag_sched* s, double* out4) {
+  if (!s || !out4) return fail(AG_ERR_VALIDATION, "null argument");
+  for (int i = 0; i < 4; ++i) out4[i] = s->host_us[i];
+  return AG_OK;
+}
+
 int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap, int64_t* n) {
   agb::DeviceGuard device_guard(s ? s->ctx->device : -1);
   if (!s || slot < 0 || slot >= s->cap || !s->live[slot]) return fail(AG_ERR_VALIDATION, "bad slot");
@@ -2164,14 +2881,9 @@ int ag_sched_viable(ag_sched* s, int32_t slot, uint32_t* out, int64_t cap, int64
   return AG_OK;
 }
 
-// Stateless beam_schedule: the context's cached session, emptied, holds
-// exactly this queue (grown when a call needs more room).
-int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int beam_width,
-                     ag_assignment* out, ag_triple* triples, int32_t triples_cap,
-                     int32_t* occupancy) {
-  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
-  if (!ctx || !q || !engines) return fail(AG_ERR_VALIDATION, "null argument");
-  if (beam_width < 1) return fail(AG_ERR_VALIDATION, "beam width < 1");
+// The context's cached session, emptied, holding exactly this queue (grown
+// when a call needs more room); cidx: container index per FIFO position.
+static int stateless_prepare(ag_ctx* ctx, const ag_queue* q, ag_sched** out, std::vector<int32_t>* cidx) {
   const int R = q->n_requests;
   if (R < 0) return fail(AG_ERR_VALIDATION, "negative request count");
   const uint64_t total = R > 0 ? (uint64_t)(q->viable_ptr[R] - q->viable_ptr[0]) : 0;
@@ -2201,12 +2913,55 @@ int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, 
   // their container index (they simply contribute no pairs)
   std::vector<int32_t> slot_to_ci(s->cap, -1);
   for (int i = 0; i < R; ++i) slot_to_ci[slots[i]] = i;
-  std::vector<int32_t> cidx(s->order.size());
-  for (size_t p = 0; p < s->order.size(); ++p) cidx[p] = slot_to_ci[s->order[p]];
+  cidx->resize(s->order.size());
+  for (size_t p = 0; p < s->order.size(); ++p) (*cidx)[p] = slot_to_ci[s->order[p]];
+  *out = s;
+  return AG_OK;
+}
+
+// Stateless beam_schedule over the context's cached session.
+int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int beam_width,
+                     ag_assignment* out, ag_triple* triples, int32_t triples_cap,
+                     int32_t* occupancy) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
+  if (!ctx || !q || !engines) return fail(AG_ERR_VALIDATION, "null argument");
+  if (beam_width < 1) return fail(AG_ERR_VALIDATION, "beam width < 1");
+  ag_sched* s = nullptr;
+  std::vector<int32_t> cidx;
+  int rc = stateless_prepare(ctx, q, &s, &cidx);
+  if (rc) return rc;
   rc = agb::run_round(s, engines, beam_width, cidx.data(), out, triples, triples_cap, occupancy);
   if (rc == AG_OK && out)
     for (int i = 0; i < out->n_triples; ++i) triples[i].slot = -1;
   return rc;
+}
+
+// Stateless audit_round_fairness(queue, engines, assignment)
+// (scheduler.cpp:456-480): the queue is installed in the context's cached
+// session (as ag_beam_schedule does) and audited on the device; triples'
+// request_index is the container index, as in the reference.
+int ag_audit_round_fairness(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int32_t n,
+                            const ag_triple* triples, uint64_t* viol_ids, int32_t* viol_agents,
+                            int32_t cap, int32_t* n_viol) {
+  agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
+  if (!ctx || !q || !engines || !n_viol || (n > 0 && !triples)) return fail(AG_ERR_VALIDATION, "null argument");
+  ag_sched* s = nullptr;
+  std::vector<int32_t> cidx;
+  int rc = stateless_prepare(ctx, q, &s, &cidx);
+  if (rc) return rc;
+  // the device queue as the host mirror holds it (no round has applied the
+  // pending ready updates / FIFO tail yet): full copies, the next round
+  // still refreshes its records from the pending lists
+  cudaStream_t st = ctx->stream;
+  const size_t Q = s->order.size();
+  if ((rc = s->d_cidx.ensure(4 * std::max<size_t>(Q, 1)))) return rc;
+  if (Q) {
+    AG_CUDA(cudaMemcpyAsync(s->d_order.p, s->order.data(), 4 * Q, cudaMemcpyHostToDevice, st));
+    AG_CUDA(cudaMemcpyAsync(s->d_cidx.p, cidx.data(), 4 * Q, cudaMemcpyHostToDevice, st));
+  }
+  AG_CUDA(cudaMemcpyAsync(s->d_ready.p, s->ready.data(), 8 * (size_t)s->cap, cudaMemcpyHostToDevice, st));
+  s->dirty_from = Q;
+  return agb::audit_impl(s, engines, n, triples, (const int32_t*)s->d_cidx.p, viol_ids, viol_agents, cap, n_viol);
 }
 
 }  // extern "C"

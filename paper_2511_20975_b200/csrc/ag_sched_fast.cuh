@@ -11,8 +11,9 @@
 // 0-3: parent 0, 4-6: parent 1, 7-8: parent 2, 9: parent 3) and holds a copy
 // of BeamState p (util, flex sum/count, skips, last history node, path
 // length, free-engine mask, one free-slot byte per engine).  A step:
-//   * the next candidate: one ballot over a cached 32-candidate window
-//     (engine masks staged by the producers) against the union of free masks;
+//   * the next candidate: one ballot over the next 32 entries of the
+//     lookahead ring (records, engine masks and histogram rows fetched ahead
+//     by warp 1) against the union of free masks;
 //   * allowed_engines (scheduler.cpp:140-156): the candidate's engine mask &
 //     the state's free mask (a re-touch -- a request with parallel ready
 //     branches -- counts survivors over the viable list instead);
@@ -102,51 +103,46 @@
   // request iff its last node was created since the walk reached it
   int q_last = -1, q_node0 = 0;
   int q_prev = -1;  // largest request index visited so far
-  int jw = -64, wlim = 0;  // candidate window [jw, jw + 32): lane l holds the mask of jw + l
-  uint32_t wm = 0;
 
-  // the next candidate whose engine mask meets a free engine of U: one
-  // ballot over the cached 32-candidate window; published windows whose mask
-  // union misses U are skipped 32 at a time
-  auto find_next = [&](uint32_t U, int& found, uint32_t& base) {
+  // the next candidate whose engine mask meets a free engine of U, from the
+  // lookahead ring (records, masks and histogram rows already in shared
+  // memory): one ballot over the next 32 ring entries; le = its ring slot.
+  // The walker's union and consumed count are published for the lookahead.
+  const int LA = A.la_rows;
+  unsigned la_tail = 0, la_head = 0;
+  auto ring_next = [&](uint32_t U, int& le, uint32_t& base) -> bool {
+    if (lane == 0) {
+      *(volatile uint32_t*)&s_U = U;
+      st_release(&s_la_tail, la_tail);  // entries before it are no longer read
+    }
     for (;;) {
-      if (j >= jw + 32) {
-        for (;;) {
-          const int w0 = j >> 5, wl = w0 + lane;
-          const bool pub = (unsigned)(wl + 1) * 32u <= have;
-          const unsigned sb = __ballot_sync(kFull, !pub || (s_wor[pub ? wl : 0] & U) != 0u);
-          if (sb == 0u) {
-            j = (w0 + 32) * 32;
-            continue;
+      if (la_tail == la_head) {
+        unsigned h = 0;
+        if (lane == 0) {
+          // every entry so far is consumed (skipped ones included): the
+          // lookahead must see the room before it can refill the ring
+          st_release(&s_la_tail, la_tail);
+          for (;;) {
+            const unsigned done = *(volatile unsigned*)&s_la_done;
+            h = *(volatile unsigned*)&s_la_head;
+            if (h > la_tail || done) break;
           }
-          const int first = __ffs(sb) - 1;
-          if (first > 0) j = (w0 + first) * 32;
-          break;
+          h = ld_acquire(&s_la_head);
         }
-        const unsigned h = wait_for((unsigned)j);
-        if (h <= (unsigned)j) return;  // producers done, list exhausted
-        jw = j & ~31;
-        const int jj = jw + lane;
-        wm = jj < (int)h ? maskf(jj) : 0u;
-        wlim = min((int)h, jw + 32);
+        la_head = __shfl_sync(kFull, h, 0);
+        if (la_head == la_tail) return false;  // list exhausted
       }
-      const unsigned b = __ballot_sync(kFull, jw + lane >= j && (wm & U) != 0u);
+      const unsigned i = la_tail + (unsigned)lane;
+      const uint32_t m = i < la_head ? s_la_mask[i & (unsigned)(LA - 1)] : 0u;
+      const unsigned b = __ballot_sync(kFull, (m & U) != 0u);
       if (b) {
         const int src = __ffs(b) - 1;
-        found = jw + src;
-        base = __shfl_sync(kFull, wm, src);
-        return;
+        le = (int)((la_tail + (unsigned)src) & (unsigned)(LA - 1));
+        base = __shfl_sync(kFull, m, src);
+        la_tail += (unsigned)src + 1u;
+        return true;
       }
-      if (wlim < jw + 32) {  // the window's tail is not published yet
-        j = wlim;
-        const unsigned h = wait_for((unsigned)j);
-        if (h <= (unsigned)j) return;
-        const int jj = jw + lane;
-        if (jj >= j && jj < (int)h) wm = maskf(jj);
-        wlim = min((int)h, jw + 32);
-        continue;
-      }
-      j = jw + 32;
+      la_tail = min(la_head, la_tail + 32u);
     }
   };
   // re-touch of state si (last node snode): counts per model of this agent
@@ -194,13 +190,12 @@
     // the heaviest such engine, unless the next one ties in utilization
     // (then flexibility, then model decide) -- otherwise every pair is a skip.
     while (!wstatus && fm) {
-      int found = -1;
+      int le = 0;
       uint32_t base = 0;
-      find_next(fm, found, base);
+      const bool got = ring_next(fm, le, base);
       AG_PHASE_TICK(0);
-      if (found < 0) break;
-      j = found + 1;
-      const Cand cr = recf(found);
+      if (!got) break;
+      const Cand cr = s_la_rec[le];
       if ((long long)cr.pos > pi) {
         sk += (int)((long long)cr.pos - pi);
         explored += (unsigned long long)((long long)cr.pos - pi);
@@ -208,9 +203,6 @@
       pi = (long long)cr.pos + 1;
       const int qcur = cr.qi, a = (int)(cr.slot_agent >> 26), slot = (int)(cr.slot_agent & 0x3ffffffu);
       const double initial = (double)cr.nvia;
-      const int hrow = found;
-      if (hrow >= rows && hrow < A.hist_cap) rows = ld_acquire(&s_rows);
-      const bool staged = hrow < rows;
       if (qcur != q_last) q_last = qcur, q_node0 = nnodes;
       const bool touched = nd >= q_node0;
       uint32_t mk = base & fm;
@@ -222,11 +214,7 @@
       }
       explored += (unsigned long long)__popc(mk);
       ++n_steps;
-      n_child += !staged;  // diagnostics: steps whose histogram row was not staged
-      auto delta_of = [&](int m) -> double {
-        if (touched) return s_rdelta[0][m];
-        return staged ? h_rat[hrow * M + m] : ratio_slow(__ldg(A.hist + ((size_t)slot * N + a) * M + m), initial);
-      };
+      auto delta_of = [&](int m) -> double { return touched ? s_rdelta[0][m] : h_rat[le * M + m]; };
       int e = __ffs(mk) - 1;
       double cu = u + sw[e];
       const uint32_t after = mk & ~((2u << e) - 1u);
@@ -245,8 +233,7 @@
       }
       AG_PHASE_TICK(1);
       const int mdl = e_model[e];
-      const uint32_t sv = touched ? (uint32_t)s_cnt[0][mdl]
-                                  : staged ? h_cnt[hrow * M + mdl] : __ldg(A.hist + ((size_t)slot * N + a) * M + mdl);
+      const uint32_t sv = touched ? (uint32_t)s_cnt[0][mdl] : h_cnt[le * M + mdl];
       if (nnodes + 1 > A.max_nodes) {
         wstatus = AG_ERR_INTERNAL + 300;  // history overflow
         break;
@@ -279,13 +266,12 @@
     const bool live = gp < nst;  // my group's state exists
     const uint32_t U = __reduce_or_sync(kFull, lead && live ? fm : 0u);
     if (!U) break;  // all-full early exit (scheduler.cpp:303-315)
-    int found = -1;
+    int le = 0;
     uint32_t base = 0;
-    find_next(U, found, base);
+    const bool got = ring_next(U, le, base);
     AG_PHASE_TICK(0);
-    if (found < 0) break;
-    j = found + 1;
-    const Cand cr = recf(found);
+    if (!got) break;
+    const Cand cr = s_la_rec[le];
     {  // whole-beam skips before this pair
       const long long k = (long long)cr.pos - pi;
       if (k > 0) {
@@ -296,9 +282,6 @@
     }
     const int qcur = cr.qi, a = (int)(cr.slot_agent >> 26), slot = (int)(cr.slot_agent & 0x3ffffffu);
     const double initial = (double)cr.nvia;
-    const int hrow = found;
-    if (hrow >= rows && hrow < A.hist_cap) rows = ld_acquire(&s_rows);
-    const bool staged = hrow < rows;
     const uint64_t key_base = tkey(qcur, a, 0);
     if (qcur != q_last) q_last = qcur, q_node0 = nnodes;
     // ---- allowed_engines (every lane of group p: state p)
@@ -321,14 +304,9 @@
     }
     explored += (unsigned long long)__reduce_add_sync(kFull, lead && live ? (mk ? __popc(mk) : 1u) : 0u);
     ++n_steps;
-    n_child += !staged;  // diagnostics: steps whose histogram row was not staged
     // flex_sum delta of a child on model m: the first-touch ratio surv /
-    // initial (staged by the producers for the head of the list), or the
-    // re-touch delta computed above
-    auto delta_of = [&](int m) -> double {
-      if (touched) return s_rdelta[gp][m];
-      return staged ? h_rat[hrow * M + m] : ratio_slow(__ldg(A.hist + ((size_t)slot * N + a) * M + m), initial);
-    };
+    // initial (fetched by the lookahead), or the re-touch delta computed above
+    auto delta_of = [&](int m) -> double { return touched ? s_rdelta[gp][m] : h_rat[le * M + m]; };
     // ---- my child: the gk-th allowed engine of state gp (or its skip child)
     const int nall = __popc(mk);
     const bool valid = live && (mk ? gk < nall : gk == 0);
@@ -482,9 +460,7 @@
         n.am = (a << 8) | mdl;
         n.prev = nd;
         n.depth = ln + 1;
-        n.nsurv = (int)(touched ? (uint32_t)s_cnt[gp][mdl]
-                                : staged ? h_cnt[hrow * M + mdl]
-                                         : __ldg(A.hist + ((size_t)slot * N + a) * M + mdl));
+        n.nsurv = (int)(touched ? (uint32_t)s_cnt[gp][mdl] : h_cnt[le * M + mdl]);
         n.nvia = cr.nvia;
         n.slot = slot;
         n.pad = 0;

@@ -108,6 +108,32 @@ def beam_schedule(device: Device, queue: Queue, engines: Engines, beam_width: in
     return _unpack(res, trip, occ, len(engines.model))
 
 
+def _ctriples(triples, slots):
+    arr = (CTriple * max(1, len(triples)))()
+    for k, ((qi, rid, a, m), sl) in enumerate(zip(triples, slots)):
+        arr[k] = CTriple(qi, a, m, sl, rid)
+    return arr
+
+
+def _audit(call, engines: Engines, triples) -> list:
+    n = len(triples)
+    arr = _ctriples(triples, [-1] * n)
+    cap = 4096
+    ids = np.zeros(cap, np.uint64)
+    ags = np.zeros(cap, np.int32)
+    nv = C.c_int32()
+    e = engines.c()
+    check(call(C.byref(e), n, arr, C.c_void_p(_ptr(ids)), C.c_void_p(_ptr(ags)), cap, C.byref(nv)))
+    return [(int(ids[i]), int(ags[i])) for i in range(min(nv.value, cap))]
+
+
+def audit_round_fairness(device: Device, queue: Queue, engines: Engines, triples) -> list:
+    """audit_round_fairness(queue, engines, assignment) (scheduler.cpp:456-480),
+    stateless: request_index is the container index of `queue`."""
+    q = queue.c()
+    return _audit(lambda *a: lib().ag_audit_round_fairness(device.handle, C.byref(q), *a), engines, triples)
+
+
 class SchedSession:
     """Resident requests (ag_sched): add -> round -> dispatch -> complete."""
 
@@ -153,6 +179,25 @@ class SchedSession:
             arr[k] = CTriple(qi, a, m, assignment.slots[i], rid)
         check(lib().ag_sched_dispatch(self._h, len(idx), arr))
 
+    def apply(self, engines: Engines, assignment: Assignment):
+        """apply_assignment (scheduler.cpp:421-454) on the session: a triple
+        whose pool is already full is stale (dropped), the rest dispatch.
+        Returns (applied flags, number applied, number stale)."""
+        n = len(assignment.triples)
+        arr = _ctriples(assignment.triples, assignment.slots or [-1] * n)
+        flags = np.zeros(max(1, n), np.uint8)
+        na, ns = C.c_int32(), C.c_int32()
+        e = engines.c()
+        check(lib().ag_sched_apply(self._h, C.byref(e), n, arr, C.c_void_p(_ptr(flags)),
+                                   C.byref(na), C.byref(ns)))
+        return flags[:n].astype(bool).tolist(), na.value, ns.value
+
+    def audit(self, engines: Engines, triples) -> list:
+        """audit_round_fairness (scheduler.cpp:456-480) of an assignment's
+        triples (request_index, request_id, agent, model) against the last
+        round's queue; returns [(RequestId, agent)] in pair order."""
+        return _audit(lambda *a: lib().ag_sched_audit(self._h, *a), engines, triples)
+
     def round_timing(self):
         """Device phase durations (us) of the last round: setup, first
         candidate chunk, walk, finalize.  Also sets walk_cycles (find, build,
@@ -167,6 +212,13 @@ class SchedSession:
         # producers' end relative to the walk's end (us; > 0: they finished later)
         self.producers_after_walk_us = (float(t[15]) - float(t[3])) / 1e3 if t[15] else 0.0
         return np.diff(t[:5].astype(np.float64)) / 1e3
+
+    def host_timing(self):
+        """Host-clock split (us) of the last round call: record preparation,
+        launch call, wait for the completion flag, result readback."""
+        t = np.zeros(4, np.float64)
+        check(lib().ag_sched_round_host_timing(self._h, C.c_void_p(_ptr(t))))
+        return t
 
     def last_round_us(self) -> float:
         """Host wall time of the last round inside the C ABI call."""

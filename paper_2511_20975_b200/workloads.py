@@ -117,6 +117,7 @@ class Config3:
         """Runs the loop; returns per-round decision latency (us) and the
         decision hash (same formula as ref_bench)."""
         weights = list(self.space.slot_throughput)
+        self.dispatch_us = []
         h = GAMMA
         lat = []
         assigned = 0
@@ -132,7 +133,14 @@ class Config3:
             h = mix(h, int(a.utilization * 1e6) & MASK, a.states_explored, a.skips & MASK)
             if on_round:
                 on_round(rd, a)
+            # Request::mark_dispatched: the prefix prune that keeps the
+            # candidate masks / histograms the next round reads current
+            # (timed to the end of its kernel: the reference rebuilds this
+            # RoundContext data inside beam_schedule, scheduler.cpp:294)
+            t2 = time.perf_counter_ns()
             self.sess.dispatch(a)
+            self.dev.synchronize()
+            self.dispatch_us.append((time.perf_counter_ns() - t2) / 1e3)
             done = []
             for (qi, rid, ag, mdl), s in zip(a.triples, a.slots):
                 self.sess.complete(s, ag)

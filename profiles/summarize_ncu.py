@@ -35,10 +35,16 @@ def full(rep, out):
     rows = list(csv.reader(io.StringIO(txt)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
+    # tensor-pipe counters (tcgen05 on sm_100a) wherever the capture has them
+    extra = [h for h in hdr if h in ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+                                     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+                                     "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+                                     "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active")]
+    metrics = RAW + extra
     agg = defaultdict(lambda: defaultdict(list))
     for r in data:
         k = short(r[col["Kernel Name"]])
-        for m in RAW:
+        for m in metrics:
             if m in col:
                 try:
                     agg[k][m].append(float(r[col[m]].replace(",", "")))

@@ -250,3 +250,179 @@ def test_beam_ties_match_oracle(walker, monkeypatch):
             assert got.utilization == want["utilization"] and got.flexibility == want["flexibility"]
             assert got.skips == want["skips"] and got.states_explored == want["states_explored"]
         del order
+
+
+def test_golden_audits(golden):
+    """audit_round_fairness on the GPU (stateless: the queue in container
+    order, ag_audit_round_fairness) against the reference's violations for
+    doctored width-4 assignments and zero for every beam output
+    (tests/golden/rounds.json, written by the unmodified reference)."""
+    cache = {}
+    n = 0
+    for j in golden("rounds.json"):
+        nn, m = j["n"], j["m"]
+        key = (nn, m, tuple(j["graph"]["depth"]))
+        if key not in cache:
+            sp = P.ConfigSpace(nn, _edges_for(nn, j["graph"]["depth"]), [1.0 + i for i in range(m)],
+                               [8.0 / 1.5 ** i for i in range(m)])
+            cache[key] = P.Device(sp)
+        dev = cache[key]
+        reqs, engs = j["requests"], j["engines"]
+        q = P.Queue(nn, [r["id"] for r in reqs], [r["arrival"] for r in reqs],
+                    [s for r in reqs for s in r["stages"]], [r["viable"] for r in reqs])
+        e = P.Engines([x["model"] for x in engs], [x["slots"] for x in engs],
+                      [x["occupancy"] for x in engs], [x["weight"] for x in engs])
+        for w, want in j["beam"].items():
+            assert len(P.audit_round_fairness(dev, q, e, [tuple(t) for t in want["triples"]])) == \
+                want["fairness_violations"]
+        for d in j["audit"]:
+            got = P.audit_round_fairness(dev, q, e, [tuple(t) for t in d["triples"]])
+            assert [list(v) for v in got] == d["violations"]
+            n += 1
+    assert n >= 120
+
+
+def test_reference_audit_and_apply_cases():
+    """scheduler_test.cpp:211-229 (the audit flags a dropped assignment) and
+    :232-265 (apply drops stale triples, a fresh round routes around the full
+    pool) on a resident session."""
+    sp = P.ConfigSpace.chain(1, 2, [1.0, 2.0], [2.0, 1.0])
+    dev = P.Device(sp)
+    sess = P.SchedSession(dev, 4, 16)
+    q = P.Queue(1, [1, 2], [0.0, 1.0], [READY, READY], [[0, 1], [0, 1]])
+    sess.add(q)
+    eng = _eng([0, 1], [2, 2], [2.0, 1.0])
+    out = sess.round(eng, 4)
+    assert len(out.triples) == 2
+    assert sess.audit(eng, out.triples) == []
+    viol = sess.audit(eng, out.triples[1:])
+    assert len(viol) == 1 and viol[0][0] == 1
+    # apply with the heavy pool filled between decision and apply
+    sp2 = P.ConfigSpace.chain(2, 2, [1.0, 2.0], [2.0, 1.0])
+    dev2 = P.Device(sp2)
+    s2 = P.SchedSession(dev2, 4, 16)
+    q2 = P.Queue(2, [1, 2], [0.0, 1.0], [READY, 0, READY, 0], [[0, 1, 2, 3], [0, 1, 2, 3]])
+    s2.add(q2)
+    e0 = _eng([0, 1], [2, 2], [2.0, 1.0])
+    a = s2.round(e0, 4)
+    assert len(a.triples) == 2
+    full = _eng([0, 1], [2, 2], [2.0, 1.0], occ=[2, 0])
+    flags, na, ns = s2.apply(full, a)
+    assert na == 0 and ns == 2 and flags == [False, False]
+    assert all(t[3] == 0 for t in a.triples)
+    retry = s2.round(full, 4)
+    flags, na, ns = s2.apply(full, retry)
+    assert ns == 0 and na == 2
+    assert all(t[3] == 1 for t in retry.triples)
+    # applied stages left the ready set: the next round has nothing to place
+    assert s2.round(_eng([0, 1], [2, 2], [2.0, 1.0]), 4).triples == []
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_session_audit_and_apply_match_oracle(seed):
+    """Resident-session rounds (chain 5 x 8, predictor sets): the audit of
+    doctored assignments against the C oracle's audit_round_fairness, and
+    apply_assignment's stale rule against a host replay, round after round."""
+    rng = np.random.default_rng(seed)
+    n, m, nreq = 5, 8, 600
+    sp = P.ConfigSpace.chain(n, m)
+    dev = P.Device(sp)
+    batch = P.AccuracyBatch.generate(sp, P.GenParams(), nreq, seed)
+    pred = P.ConfigPredictor(dev)
+    pr = pred.predict_batch(batch.to_device(), P.OracleRouter(0.001))
+    torch.cuda.synchronize()
+    nv = pr.n_viable.cpu().numpy()
+    vv = pr.viable.cpu().numpy().view(np.uint32)
+    reqs = [dict(id=int(r), arrival=float(r // 2), stages=[READY] + [0] * (n - 1),
+                 viable=[int(x) for x in vv[r, : nv[r]]]) for r in range(nreq)]
+    sess = P.SchedSession(dev, nreq, sum(len(r["viable"]) for r in reqs) + 1)
+    slots = sess.add(P.Queue(n, [r["id"] for r in reqs], [r["arrival"] for r in reqs],
+                             [s for r in reqs for s in r["stages"]], [r["viable"] for r in reqs]))
+    by_slot = {int(s): reqs[i] for i, s in enumerate(slots)}
+    weights = [8.0 / 1.5 ** i for i in range(m)]
+    for rnd in range(6):
+        caps = [int(rng.integers(2, 6)) for _ in range(m)]
+        occ = [int(rng.integers(0, c + 1)) for c in caps]
+        eng = P.Engines(list(range(m)), caps, occ, weights)
+        a = sess.round(eng, 4)
+        queue_slots = [s for s in sorted(by_slot, key=lambda s: (by_slot[s]["arrival"], by_slot[s]["id"]))
+                       if READY in by_slot[s]["stages"]]
+        qr = [by_slot[s] for s in queue_slots]
+        qd = O.QueueData(n, m, sp.depth.tolist(), sp.decl.tolist(), [r["id"] for r in qr],
+                         [r["arrival"] for r in qr], [s for r in qr for s in r["stages"]],
+                         [r["viable"] for r in qr], eng.model, eng.slots, eng.occupancy, eng.weight)
+        T = len(a.triples)
+        docs = [a.triples, a.triples[1:], a.triples[: T // 2], []]
+        if T >= 2:
+            docs.append([a.triples[1], a.triples[0]] + a.triples[2:])
+        for d in docs:
+            assert sess.audit(eng, d) == O.audit_round_fairness(qd, d)
+        # apply against pools that lost some free slots since the decision
+        later = [min(c, o + int(rng.integers(0, 2))) for c, o in zip(caps, occ)]
+        leng = P.Engines(list(range(m)), caps, later, weights)
+        flags, na, ns = sess.apply(leng, a)
+        left = [c - o for c, o in zip(caps, later)]
+        want = []
+        for t in a.triples:
+            ok = left[t[3]] > 0
+            left[t[3]] -= ok
+            want.append(ok)
+        assert flags == want and na == sum(want) and ns == T - sum(want)
+        for (qi, rid, ag, mdl), s, ok in zip(a.triples, a.slots, flags):
+            if ok:
+                r = by_slot[s]
+                r["stages"][ag] = 2
+                r["viable"] = [int(x) for x in O.prefix_prune(n, m, r["viable"], ag, mdl)]
+                sess.complete(s, ag)
+                r["stages"][ag] = 3
+                if ag + 1 < n:
+                    r["stages"][ag + 1] = READY
+        for s in list(by_slot)[:40]:
+            assert sess.viable(s).tolist() == by_slot[s]["viable"]
+
+
+def test_session_pool_is_a_capacity():
+    """max_configs bounds the viable lists resident at once, not every list
+    the session ever adds: continuous add / dispatch (prefix prune) / remove
+    cycles through a pool ~4x smaller than the total added, with the live
+    lists packed on the device when an add does not fit."""
+    rng = np.random.default_rng(7)
+    n, m = 3, 4
+    sp = P.ConfigSpace.chain(n, m)
+    dev = P.Device(sp)
+    sess = P.SchedSession(dev, 40, 600)
+    mirror = {}
+    next_id = 0
+    added = 0
+    for it in range(40):
+        k = 8
+        reqs = []
+        for _ in range(k):
+            v = sorted(set(int(x) for x in rng.integers(0, sp.size, int(rng.integers(5, 25)))))
+            reqs.append(dict(id=next_id, arrival=float(next_id), stages=[READY, 0, 0], viable=v))
+            next_id += 1
+        added += sum(len(r["viable"]) for r in reqs)
+        slots = sess.add(P.Queue(n, [r["id"] for r in reqs], [r["arrival"] for r in reqs],
+                                 [s for r in reqs for s in r["stages"]], [r["viable"] for r in reqs]))
+        for s, r in zip(slots, reqs):
+            mirror[int(s)] = r
+        # prune some of them in place (agent 0, a candidate model)
+        trip, tslots = [], []
+        for s in list(mirror)[-k:]:
+            r = mirror[s]
+            mdl = int((r["viable"][0] // m ** (n - 1)) % m)
+            trip.append((0, r["id"], 0, mdl))
+            tslots.append(s)
+            r["viable"] = [int(x) for x in O.prefix_prune(n, m, r["viable"], 0, mdl)]
+            r["stages"][0] = 2
+        sess.dispatch(P.Assignment(trip, [], 0.0, 0.0, 0, 0, tslots))
+        # the oldest leave
+        old = sorted(mirror)[:k] if len(mirror) > 24 else []
+        old = sorted(mirror, key=lambda s: mirror[s]["id"])[:k] if len(mirror) > 24 else []
+        if old:
+            sess.remove(old)
+            for s in old:
+                del mirror[s]
+        for s, r in mirror.items():
+            assert sess.viable(s).tolist() == r["viable"], (it, s)
+    assert added > 4 * 600
