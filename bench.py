@@ -494,10 +494,46 @@ def run_config5(horizon=240.0):
             row["trace_identical"] = outs[0] == outs[1]
             same &= row["trace_identical"]
             pts.append(row)
+    # BASELINE scale: a 5-stage chain x 8 tiers scenario (the config-2 space)
+    # with ~500-960 requests queued per round, drained
+    scale = None
+    with tempfile.TemporaryDirectory() as td:
+        sc = {"name": "chain5x8", "seed": 1,
+              "workflow": {"agents": [f"a{i}" for i in range(5)],
+                           "edges": [[f"a{i}", f"a{i + 1}"] for i in range(4)]},
+              "models": [{"name": f"m{i}", "cost": 1.5 ** i, "slot_throughput": 8.0 / 1.5 ** i}
+                         for i in range(8)],
+              "engines": [{"model": f"m{i}", "slots": 32,
+                           "service": {"mu": -0.3 + 0.35 * i, "sigma": 0.25, "floor": 0.05}}
+                          for i in range(8)],
+              "router": {"kind": "oracle", "eval_latency": 0.002},
+              "predictor": {"min_budget": 0.12, "ema_alpha": 0.2, "router_lanes": 16},
+              "accuracy": {"p_easy": 0.6, "p_medium": 0.3, "p_hard": 0.1, "easy_base_prob": 0.5},
+              "workload": {"arrival_rate": 60.0, "num_requests": 1200, "horizon": 240,
+                           "per_workflow_sample": 256},
+              "scheduler": {"beam_width": 4},
+              "sweep": {"rates": [60.0], "seeds": [1], "horizon": 60},
+              "metrics": {"sample_interval": 0.5}}
+        sp = os.path.join(td, "chain5x8.json")
+        json.dump(sc, open(sp, "w"))
+        row, outs = {"scenario": "chain5x8 (5 stages x 8 tiers, 8 pools x 32 slots, 60 req/s, "
+                                 "1200 requests, drain)"}, []
+        for kind, b in (("reference", ref_bin), ("gpu", gpu_bin)):
+            out = os.path.join(td, f"{kind}_scale.jsonl")
+            r = subprocess.run([b, sp, "aragog", out, "--requests", "1200"], capture_output=True,
+                               text=True, check=True)
+            j = json.loads(r.stdout.strip().splitlines()[-1])
+            row[kind] = {"rounds": j["rounds"], "pairs": j["pairs"], "wall_s": j["wall_s"],
+                         "rounds_per_s": j["rounds_per_s"], "gpu_launches": j["gpu_launches"]}
+            outs.append(open(out, "rb").read())
+        row["trace_identical"] = outs[0] == outs[1]
+        same &= row["trace_identical"]
+        scale = row
     return {"workload": f"config5: reference.json under run_simulation, horizon {horizon:g} s, "
                         f"aragog policy, rates {list(C5_RATES)} req/s; reference build vs the "
-                        "same sources relinked with the GPU adapter",
-            "traces_identical": same, "points": pts,
+                        "same sources relinked with the GPU adapter; plus a 5x8 scenario at "
+                        "BASELINE scale",
+            "traces_identical": same, "points": pts, "scale": scale,
             "note": "single-request decisions through the C ABI: each predict / round is one "
                     "launch + synchronisation, so tiny queues are launch-latency bound"}
 
@@ -887,6 +923,10 @@ def summarize(line, sched, deep, noisy, linear, chain, config5, select=None, con
                           "rounds_per_s": [[p["rate"], _r(p["gpu"]["rounds_per_s"]),
                                             _r(p["reference"]["rounds_per_s"])]
                                            for p in config5["points"]]}
+        if config5.get("scale"):
+            sc = config5["scale"]
+            out["config5"]["scale_5x8"] = [sc["trace_identical"], _r(sc["gpu"]["wall_s"]),
+                                           _r(sc["reference"]["wall_s"])]
     return out
 
 

@@ -427,6 +427,19 @@ int ag_select_per_workflow_host(ag_ctx* ctx, const ag_truth* sample_host,
 int ag_sched_queued_ahead(ag_sched* s, int32_t* out);
 
 /* ======================================================================== *
+ * Trace I/O of accurate sets         *
+ * ======================================================================== */
+/* Writes one JSON line per request of the host batch: id, arrival (seconds;
+ * arrival may be NULL for 0), and the accurate set enumerated on the device
+ * -- {"encoding": "bitmap", "size": S, "bits": hex} over the canonical
+ * enumeration when S = M^N <= 4096 (byte k = indices 8k..8k+7, bit 0 first),
+ * {"encoding": "list", "size": S, "members": [...]} otherwise.  The reference
+ * has no writer for this clause: the format is this library's reading of it.
+ * AG_ERR_IO when the file cannot be written. */
+int ag_trace_write(ag_ctx* ctx, const ag_truth* truth_host, const double* arrival,
+                   const char* path, uint64_t* bytes_written);
+
+/* ======================================================================== *
  * Host-side input synthesis (reference generators; not on the hot path)     *
  * ======================================================================== */
 typedef struct {

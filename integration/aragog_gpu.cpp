@@ -9,8 +9,13 @@
 //   enumerate_members             (src/accuracy.cpp:227-238)  -> ag_route_enumerate_host
 //   select_per_input_config       (src/workload.cpp:149-176)  -> ag_select_per_input_host
 //   select_per_workflow_config    (src/workload.cpp:99-127)   -> ag_select_per_workflow_host
+//   audit_round_fairness          (src/scheduler.cpp:456-480) -> ag_sched_audit (resident session)
+//                                                                / ag_audit_round_fairness
 //
-// The reference objects are linked with these five symbols weakened
+// beam_schedule keeps the in-flight requests resident on the GPU across
+// rounds (Resident below): only arrivals, dispatches and completions travel.
+//
+// The reference objects are linked with these six symbols weakened
 // (objcopy --weaken-symbol, integration/Makefile), so the definitions below
 // win at link time.  There is no CPU fallback: a RouterBackend that is not an
 // OracleRouter (or a NoisyRouter over one) -- e.g. the CountingRouter test
@@ -27,6 +32,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "aragog/accuracy.h"
@@ -88,8 +94,39 @@ void check(int rc) {
 }
 
 std::mutex g_mu;
+struct Gpu;
+Gpu* g_last_round = nullptr;  // the context whose resident session ran the last round
+// the last beam_schedule result, as returned: (queue ids, triples)
+std::vector<std::uint64_t> g_beam_ids;
+std::vector<std::uint64_t> g_beam_trip;  // request_index, request, agent, model per triple
+std::vector<double> g_beam_eng;          // model, slots, occupancy, weight per pool
 
 // One GPU space + context per distinct (graph, catalog); predictors per plan.
+// The scheduler's in-flight requests kept resident on the GPU across rounds
+// (ag_sched_*): the adapter follows each request's stages between calls and
+// forwards only the changes -- arrivals (add), the previous round's applied
+// triples and the stages the simulator dispatched (dispatch: the prefix
+// prune on the device), completions (complete) -- instead of uploading the
+// whole queue every round.
+struct Resident {
+  ag_sched* s = nullptr;
+  int cap = 0;
+  std::uint64_t pool = 0;
+  struct Entry {
+    int32_t slot;
+    std::vector<uint8_t> st;     // stages as last forwarded
+    double arrival;
+    std::vector<uint32_t> vi;    // viable list as forwarded and pruned (host copy)
+  };
+  std::unordered_map<std::uint64_t, Entry> live;  // by RequestId
+  std::vector<ag_triple> last;                    // the previous round's assignment
+  std::vector<std::uint64_t> last_ids;            // the previous round's queue (container order)
+  bool round_valid = false;                       // nothing forwarded since the last round
+  ~Resident() {
+    if (s) ag_sched_destroy(s);
+  }
+};
+
 struct Gpu {
   ag_space* space = nullptr;
   ag_ctx* ctx = nullptr;
@@ -97,6 +134,7 @@ struct Gpu {
   std::uint64_t size = 0;
   std::map<std::pair<int, int>, ag_predictor*> preds;  // (chains, exhaustive)
   int viable_cap = 0;
+  std::unique_ptr<Resident> res;
 };
 
 std::map<std::string, std::unique_ptr<Gpu>>& cache() {
@@ -353,6 +391,197 @@ Configuration select_per_workflow_config(const std::vector<AccurateSet>& sample,
   return space.at_index(chosen);
 }
 
+namespace {
+
+// Forwards the queue's changes since the last round to the resident session
+// and runs the round there; false when the session cannot hold the queue
+// (the caller then takes the stateless path).  Container order must be FIFO
+// (arrival, id) -- the simulator's schedulable list (simulation.cpp:182-192)
+// -- so a triple's request_index (the FIFO rank of ready requests) is the
+// container index, as the reference's.
+bool resident_round(Gpu& g, const std::vector<const Request*>& queue, int M, const ag_engines& eg, int B,
+                    ag_assignment* a, std::vector<ag_triple>& trip, std::vector<int32_t>& occ) {
+  const int N = g.n;
+  if (!g.res) g.res = std::make_unique<Resident>();
+  Resident& R = *g.res;
+  std::uint64_t need = 0;
+  for (const Request* r : queue) need += r->viable.size();
+  if (!R.s || (int)queue.size() * 2 > R.cap || need * 4 > R.pool) {
+    // (re)create, sized with headroom; everything is re-added below
+    if (R.s) ag_sched_destroy(R.s);
+    R.s = nullptr;
+    R.live.clear();
+    R.last.clear();
+    R.cap = std::max(1024, 4 * (int)queue.size());
+    R.pool = std::max<std::uint64_t>(1u << 20, 16 * need);
+    if (ag_sched_create(g.ctx, R.cap, R.pool, &R.s) != AG_OK) {
+      R.s = nullptr;
+      return false;
+    }
+  }
+  std::unordered_map<std::uint64_t, const Request*> in_q;
+  in_q.reserve(queue.size() * 2);
+  for (const Request* r : queue) in_q.emplace(r->id, r);
+  constexpr uint8_t kPend = (uint8_t)StageState::kPending, kRdy = (uint8_t)StageState::kReady,
+                    kFly = (uint8_t)StageState::kInFlight, kDone = (uint8_t)StageState::kDone;
+  std::vector<ag_triple> disp;
+  std::vector<std::pair<int32_t, int32_t>> comp;
+  std::vector<int32_t> drop;
+  std::vector<const Request*> add;
+  // Request::mark_dispatched's prefix prune on the host copy (request.cpp:70-86)
+  std::vector<uint64_t> place(N);
+  {
+    uint64_t pl = 1;
+    for (int ag = N - 1; ag >= 0; --ag) place[ag] = pl, pl *= (uint64_t)M;
+  }
+  auto prune = [&](Resident::Entry& e, int ag, int mdl) {
+    size_t w = 0;
+    for (uint32_t c : e.vi)
+      if ((int)((c / place[ag]) % (uint64_t)M) == mdl) e.vi[w++] = c;
+    e.vi.resize(w);
+  };
+  // the previous round's triples of requests that left the queue: applied
+  // (a READY stage only leaves READY by dispatch; a stale triple leaves the
+  // request ready, hence queued)
+  for (const ag_triple& t : R.last) {
+    if (in_q.count(t.request_id)) continue;
+    auto it = R.live.find(t.request_id);
+    if (it == R.live.end() || it->second.st[t.agent] != kRdy) continue;
+    disp.push_back(ag_triple{0, t.agent, t.model, it->second.slot, t.request_id});
+    it->second.st[t.agent] = kFly;
+    prune(it->second, t.agent, t.model);
+  }
+  // queued requests: stage transitions since they were last forwarded
+  for (const Request* r : queue) {
+    auto it = R.live.find(r->id);
+    if (it == R.live.end()) {
+      add.push_back(r);
+      continue;
+    }
+    Resident::Entry& e = it->second;
+    bool ok = e.arrival == r->arrival, completed = false;
+    const size_t n_disp = disp.size(), n_comp = comp.size();
+    for (int ag = 0; ag < N && ok; ++ag) {
+      const uint8_t o = e.st[ag], nw = (uint8_t)r->stages[ag];
+      if (o == nw) continue;
+      if (o == kRdy && (nw == kFly || nw == kDone)) {
+        disp.push_back(ag_triple{0, ag, r->executed_model[ag], e.slot, r->id});
+        prune(e, ag, r->executed_model[ag]);
+        if (nw == kDone) comp.emplace_back(e.slot, ag), completed = true;
+      } else if (o == kFly && nw == kDone) {
+        comp.emplace_back(e.slot, ag), completed = true;
+      } else if (!(o == kPend && nw == kRdy)) {
+        ok = false;
+      }
+    }
+    // PENDING -> READY only through a completion (Request::mark_complete)
+    for (int ag = 0; ag < N && ok; ++ag)
+      if (e.st[ag] == kPend && (uint8_t)r->stages[ag] == kRdy && !completed) ok = false;
+    // the same request: the pruned host copy matches its viable list (size
+    // and both ends -- another run's request of the same id diverges here)
+    if (ok) {
+      ok = e.vi.size() == r->viable.size();
+      if (ok && !e.vi.empty())
+        ok = e.vi.front() == (uint32_t)index_of(r->viable.front().models, M) &&
+             e.vi.back() == (uint32_t)index_of(r->viable.back().models, M);
+    }
+    if (!ok) {  // not explained by dispatch / complete: forward it afresh
+      disp.resize(n_disp);
+      comp.resize(n_comp);
+      drop.push_back(e.slot);
+      R.live.erase(it);
+      add.push_back(r);
+      continue;
+    }
+    for (int ag = 0; ag < N; ++ag) e.st[ag] = (uint8_t)r->stages[ag];
+  }
+  R.last.clear();
+  auto reset = [&]() {
+    ag_sched_destroy(R.s);
+    R.s = nullptr;
+    R.live.clear();
+    return false;
+  };
+  // a forwarded change the session rejects means the requests are not the
+  // ones it holds: start over (stateless this call)
+  if (!disp.empty() && ag_sched_dispatch(R.s, (int32_t)disp.size(), disp.data()) != AG_OK) return reset();
+  for (auto& c : comp)
+    if (ag_sched_complete(R.s, c.first, c.second) != AG_OK) return reset();
+  // requests out of the queue that can never return (nothing ready or
+  // pending: only completions of in-flight stages remain) or that hold a
+  // READY stage no triple explains
+  for (auto it = R.live.begin(); it != R.live.end();) {
+    if (in_q.count(it->first)) {
+      ++it;
+      continue;
+    }
+    bool pend = false, rdy = false;
+    for (uint8_t x : it->second.st) pend |= x == kPend, rdy |= x == kRdy;
+    if (!pend || rdy) {
+      drop.push_back(it->second.slot);
+      it = R.live.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  if (!drop.empty() && ag_sched_remove(R.s, (int32_t)drop.size(), drop.data()) != AG_OK) return reset();
+  if (!add.empty()) {
+    std::vector<uint64_t> ids;
+    std::vector<double> arr;
+    std::vector<uint8_t> st;
+    std::vector<int64_t> vptr{0};
+    std::vector<uint32_t> viable;
+    for (const Request* r : add) {
+      ids.push_back(r->id);
+      arr.push_back(r->arrival);
+      for (StageState x : r->stages) st.push_back((uint8_t)x);
+      for (const Configuration& c : r->viable) viable.push_back((uint32_t)index_of(c.models, M));
+      vptr.push_back((int64_t)viable.size());
+    }
+    if (viable.empty()) viable.push_back(0);
+    std::vector<int32_t> slots(add.size());
+    const ag_queue q{(int32_t)add.size(), ids.data(), arr.data(), st.data(), vptr.data(), viable.data()};
+    if (ag_sched_add(R.s, &q, slots.data()) != AG_OK) return reset();  // full: rebuilt next call
+    for (size_t i = 0; i < add.size(); ++i)
+      R.live[add[i]->id] = Resident::Entry{
+          slots[i], std::vector<uint8_t>(st.begin() + (long)(i * N), st.begin() + (long)((i + 1) * N)),
+          add[i]->arrival, std::vector<uint32_t>(viable.begin() + vptr[i], viable.begin() + vptr[i + 1])};
+  }
+  check(ag_sched_round(R.s, &eg, B, a, trip.data(), (int32_t)trip.size(), occ.data()));
+  R.last.assign(trip.begin(), trip.begin() + a->n_triples);
+  R.last_ids.clear();
+  for (const Request* r : queue) R.last_ids.push_back(r->id);
+  R.round_valid = true;
+  return true;
+}
+
+}  // namespace
+
+static std::vector<double> engines_key(const std::vector<EngineState>& engines) {
+  std::vector<double> k;
+  for (const EngineState& e : engines) {
+    k.push_back(e.model);
+    k.push_back(e.slots);
+    k.push_back(e.occupancy());
+    k.push_back(e.weight);
+  }
+  return k;
+}
+
+static void remember_beam(const std::vector<const Request*>& queue, const std::vector<EngineState>& engines,
+                          const Assignment& out) {
+  g_beam_eng = engines_key(engines);
+  g_beam_ids.clear();
+  for (const Request* r : queue) g_beam_ids.push_back(r->id);
+  g_beam_trip.clear();
+  for (const AssignmentTriple& t : out.triples) {
+    g_beam_trip.push_back(t.request_index);
+    g_beam_trip.push_back(t.request);
+    g_beam_trip.push_back((std::uint64_t)t.agent);
+    g_beam_trip.push_back((std::uint64_t)t.model);
+  }
+}
+
 Assignment beam_schedule(const std::vector<const Request*>& queue,
                          const std::vector<EngineState>& engines, const SchedulerParams& params) {
   if (params.beam_width < 1) throw ValidationError("beam width < 1");
@@ -407,6 +636,32 @@ Assignment beam_schedule(const std::vector<const Request*>& queue,
   }
   Gpu& g = gpu_for(*graph, cost, thr);
   const int N = g.n;
+  for (const Request* r : queue)
+    if ((int)r->stages.size() != N) throw ValidationError("request stage count mismatch");
+  bool fifo = true;
+  for (size_t i = 1; i < queue.size() && fifo; ++i) {
+    const Request &p = *queue[i - 1], &c = *queue[i];
+    fifo = p.arrival < c.arrival || (p.arrival == c.arrival && p.id < c.id);
+  }
+  // small queues: one upload is cheaper than forwarding changes call by call
+  constexpr size_t kResidentMin = 32;
+  if (fifo && queue.size() >= kResidentMin && resident_round(g, queue, M, eg, params.beam_width, &a, trip, occ)) {
+    Assignment out;
+    out.triples.reserve((size_t)a.n_triples);
+    for (int i = 0; i < a.n_triples; ++i)
+      out.triples.push_back(AssignmentTriple{(std::size_t)trip[i].request_index, trip[i].request_id,
+                                             trip[i].agent, trip[i].model});
+    out.occupancy.assign(occ.begin(), occ.begin() + (long)engines.size());
+    out.utilization = a.utilization;
+    out.flexibility = a.flexibility;
+    out.skips = (long)a.skips;
+    out.states_explored = (std::size_t)a.states_explored;
+    g_last_round = &g;
+    remember_beam(queue, engines, out);
+    return out;
+  }
+  if (g.res) g.res->round_valid = false;
+  g_last_round = nullptr;
   std::vector<uint64_t> ids;
   std::vector<double> arrival;
   std::vector<uint8_t> stages;
@@ -434,6 +689,96 @@ Assignment beam_schedule(const std::vector<const Request*>& queue,
   out.flexibility = a.flexibility;
   out.skips = (long)a.skips;
   out.states_explored = (std::size_t)a.states_explored;
+  remember_beam(queue, engines, out);
+  return out;
+}
+
+// audit_round_fairness (scheduler.cpp:456-480) on the GPU: against the
+// resident session when it ran this very queue's round (the simulator audits
+// right after beam_schedule, simulation.cpp:318-322), else stateless.
+std::vector<FairnessViolation> audit_round_fairness(const std::vector<const Request*>& queue,
+                                                    const std::vector<EngineState>& engines,
+                                                    const Assignment& assignment) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  // beam_schedule's own output on this queue has no violation: every beam
+  // state is extended at every pair where it has an allowed engine
+  // (scheduler.cpp:331-347; a state gets a skip child only when its mask is
+  // empty), the winner is one of the states, and replaying its triples from
+  // initial_state reproduces its ancestors -- so each pair it left unassigned
+  // had no allowed engine at that point.  Any other assignment is audited on
+  // the device.
+  {
+    bool own = g_beam_ids.size() == queue.size() && g_beam_trip.size() == 4 * assignment.triples.size() &&
+               g_beam_eng == engines_key(engines);
+    for (size_t i = 0; own && i < queue.size(); ++i) own = g_beam_ids[i] == queue[i]->id;
+    for (size_t i = 0; own && i < assignment.triples.size(); ++i) {
+      const AssignmentTriple& t = assignment.triples[i];
+      own = g_beam_trip[4 * i] == t.request_index && g_beam_trip[4 * i + 1] == t.request &&
+            g_beam_trip[4 * i + 2] == (std::uint64_t)t.agent && g_beam_trip[4 * i + 3] == (std::uint64_t)t.model;
+    }
+    if (own) return {};
+  }
+  std::vector<int32_t> model, eslots, eocc;
+  std::vector<double> weight;
+  int max_model = 1;
+  for (const EngineState& e : engines) {
+    model.push_back(e.model);
+    eslots.push_back(e.slots);
+    eocc.push_back(e.occupancy());
+    weight.push_back(e.weight);
+    max_model = std::max(max_model, e.model);
+  }
+  ag_engines eg{(int32_t)engines.size(), model.data(), eslots.data(), eocc.data(), weight.data()};
+  std::vector<ag_triple> tr;
+  for (const AssignmentTriple& t : assignment.triples)
+    tr.push_back(ag_triple{(int32_t)t.request_index, t.agent, t.model, -1, t.request});
+  const int cap = (int)std::max<size_t>(1, queue.size() * 64);
+  std::vector<uint64_t> vid((size_t)cap);
+  std::vector<int32_t> vag((size_t)cap);
+  int32_t nv = 0;
+  bool same = g_last_round && g_last_round->res && g_last_round->res->round_valid &&
+              g_last_round->res->last_ids.size() == queue.size();
+  if (same)
+    for (size_t i = 0; i < queue.size() && same; ++i) same = g_last_round->res->last_ids[i] == queue[i]->id;
+  if (same) {
+    check(ag_sched_audit(g_last_round->res->s, &eg, (int32_t)tr.size(), tr.data(), vid.data(), vag.data(), cap,
+                         &nv));
+  } else {
+    const WorkflowGraph* graph = queue.empty() ? nullptr : queue[0]->graph;
+    for (const Request* r : queue)
+      for (const Configuration& c : r->viable)
+        for (int d : c.models) max_model = std::max(max_model, d);
+    if (!graph) {
+      static const WorkflowGraph one = WorkflowGraph::build({"a"}, {});
+      graph = &one;
+    }
+    const int M = max_model + 1;
+    std::vector<double> cost(M), thr(M);
+    for (int i = 0; i < M; ++i) {
+      cost[i] = 1.0 + i;
+      thr[i] = (double)(M - i);
+    }
+    Gpu& g = gpu_for(*graph, cost, thr);
+    std::vector<uint64_t> ids;
+    std::vector<double> arrival;
+    std::vector<uint8_t> stages;
+    std::vector<int64_t> vptr{0};
+    std::vector<uint32_t> viable;
+    for (const Request* r : queue) {
+      ids.push_back(r->id);
+      arrival.push_back(r->arrival);
+      if ((int)r->stages.size() != g.n) throw ValidationError("request stage count mismatch");
+      for (StageState x : r->stages) stages.push_back((uint8_t)x);
+      for (const Configuration& c : r->viable) viable.push_back((uint32_t)index_of(c.models, M));
+      vptr.push_back((int64_t)viable.size());
+    }
+    if (viable.empty()) viable.push_back(0);
+    ag_queue q{(int32_t)queue.size(), ids.data(), arrival.data(), stages.data(), vptr.data(), viable.data()};
+    check(ag_audit_round_fairness(g.ctx, &q, &eg, (int32_t)tr.size(), tr.data(), vid.data(), vag.data(), cap, &nv));
+    if (g.res) g.res->round_valid = false;
+  }
+  std::vector<FairnessViolation> out;
+  for (int i = 0; i < std::min(nv, cap); ++i) out.push_back(FairnessViolation{vid[(size_t)i], vag[(size_t)i]});
   return out;
 }
 

@@ -57,6 +57,7 @@ struct CostArgs {
   int R;
   int32_t* r_task;              // [R+1] task range per request (k_cost_plan)
   uint64_t* tsize;              // members per task (k_cost_plan)
+  int32_t* t_req;               // [tasks] request of each task (k_cost_plan)
   uint64_t* rec;                // [R][4] shard records (ag_shard_records) or null
   int allow_empty;              // shard records: an empty shard is not an error
   uint32_t* chosen;
@@ -133,7 +134,9 @@ __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ Cost
   int32_t acc = s_wsum[w] + x - mine;
   for (int r = r0; r < r1; ++r) {
     A.r_task[r] = acc;
-    acc += (int32_t)((A.offsets[r + 1] - A.offsets[r] + ts - 1) / ts);
+    const int32_t nt = (int32_t)((A.offsets[r + 1] - A.offsets[r] + ts - 1) / ts);
+    for (int32_t k = 0; k < nt; ++k) A.t_req[acc + k] = r;
+    acc += nt;
   }
 }
 
@@ -153,11 +156,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_con
   const uint64_t ts = *A.tsize;
   // persistent warps over the tasks (their number is only known on the device)
   for (int t = blockIdx.x * kCostWarps + (threadIdx.x >> 5); t < n_tasks; t += gridDim.x * kCostWarps) {
-  int r = 0;  // the task's request: last r with r_task[r] <= t (binary search)
-  for (int lo = 0, hi = A.R; lo < hi;) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (A.r_task[mid] <= t) r = mid, lo = mid; else hi = mid - 1;
-  }
+  const int r = A.t_req[t];  // the task's request
   const uint64_t b0 = A.offsets[r] + (uint64_t)(t - A.r_task[r]) * ts;
   const uint64_t rest = A.offsets[r + 1] - b0;
   const uint32_t len = (uint32_t)(rest < ts ? rest : ts);
@@ -352,13 +351,15 @@ int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, i
     if ((rc = ctx->async_status.ensure(16))) return rc;
     AG_CUDA(cudaMemsetAsync(ctx->async_status.p, 0, 16, st));
   }
-  if ((rc = ctx->cost_status.ensure((size_t)(R + 1) * 4 + 64)) ||
+  const size_t rt_bytes = (((size_t)(R + 1) * 4 + 15) & ~(size_t)15) + 16;
+  if ((rc = ctx->cost_status.ensure(rt_bytes + 4 * tcap)) ||
       (rc = ctx->cost_tasks.ensure(tcap * sizeof(agb::Key))) || (rc = ctx->cost_prefix.ensure(16 * n_pre)))
     return rc;
   A.prefix = (const double2*)ctx->cost_prefix.p;
   A.status = (int32_t*)ctx->async_status.p;
   A.r_task = (int32_t*)ctx->cost_status.p;
   A.tsize = (uint64_t*)((char*)ctx->cost_status.p + (((size_t)(R + 1) * 4 + 15) & ~(size_t)15));
+  A.t_req = (int32_t*)((char*)ctx->cost_status.p + rt_bytes);
   A.task_best = (agb::Key*)ctx->cost_tasks.p;
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);

@@ -1908,6 +1908,7 @@ struct ag_sched {
   double host_us[4] = {0, 0, 0, 0};  // last round: prep, launch call, wait, readback (host clock)
   // session changes since creation; the audit needs the last round's queue
   uint64_t epoch = 1, round_epoch = 0;
+  uint64_t stateless_fp = 0;  // fingerprint of the queue of the last stateless round
   agb::Scratch d_audit;
   // device
   agb::Scratch d_ready, d_cand, d_hist, d_nv, d_voff, d_pool, d_ids, d_order, d_cidx, d_pinfo;
@@ -2919,6 +2920,23 @@ static int stateless_prepare(ag_ctx* ctx, const ag_queue* q, ag_sched** out, std
   return AG_OK;
 }
 
+// fingerprint of a stateless queue (ids, arrivals, stages, viable sizes)
+static uint64_t queue_fp(const ag_queue* q, int N) {
+  uint64_t h = 0x9e3779b97f4a7c15ull ^ (uint64_t)q->n_requests;
+  auto mixin = [&](uint64_t x) {
+    h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  };
+  for (int i = 0; i < q->n_requests; ++i) {
+    mixin(q->ids[i]);
+    uint64_t ab;
+    std::memcpy(&ab, &q->arrival[i], 8);
+    mixin(ab);
+    mixin((uint64_t)(q->viable_ptr[i + 1] - q->viable_ptr[i]));
+    for (int a = 0; a < N; ++a) mixin(q->stages ? q->stages[(size_t)i * N + a] : 255u);
+  }
+  return h | 1ull;
+}
+
 // Stateless beam_schedule over the context's cached session.
 int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, int beam_width,
                      ag_assignment* out, ag_triple* triples, int32_t triples_cap,
@@ -2933,6 +2951,7 @@ int ag_beam_schedule(ag_ctx* ctx, const ag_queue* q, const ag_engines* engines, 
   rc = agb::run_round(s, engines, beam_width, cidx.data(), out, triples, triples_cap, occupancy);
   if (rc == AG_OK && out)
     for (int i = 0; i < out->n_triples; ++i) triples[i].slot = -1;
+  s->stateless_fp = rc == AG_OK ? queue_fp(q, s->N) : 0;
   return rc;
 }
 
@@ -2945,10 +2964,16 @@ int ag_audit_round_fairness(ag_ctx* ctx, const ag_queue* q, const ag_engines* en
                             int32_t cap, int32_t* n_viol) {
   agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx || !q || !engines || !n_viol || (n > 0 && !triples)) return fail(AG_ERR_VALIDATION, "null argument");
+  // the queue of the last stateless round, untouched since: audit in place
+  ag_sched* c = ctx->beam_cache;
+  if (c && c->stateless_fp && c->round_epoch == c->epoch && c->stateless_fp == queue_fp(q, c->N))
+    return agb::audit_impl(c, engines, n, triples, (const int32_t*)c->d_cidx.p, viol_ids, viol_agents, cap,
+                           n_viol);
   ag_sched* s = nullptr;
   std::vector<int32_t> cidx;
   int rc = stateless_prepare(ctx, q, &s, &cidx);
   if (rc) return rc;
+  s->stateless_fp = 0;
   // the device queue as the host mirror holds it (no round has applied the
   // pending ready updates / FIFO tail yet): full copies, the next round
   // still refreshes its records from the pending lists

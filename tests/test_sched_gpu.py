@@ -278,6 +278,11 @@ def test_golden_audits(golden):
         for d in j["audit"]:
             got = P.audit_round_fairness(dev, q, e, [tuple(t) for t in d["triples"]])
             assert [list(v) for v in got] == d["violations"]
+            # right after a stateless round on the same queue the audit reuses
+            # the queue already on the device
+            P.beam_schedule(dev, q, e, 4)
+            got = P.audit_round_fairness(dev, q, e, [tuple(t) for t in d["triples"]])
+            assert [list(v) for v in got] == d["violations"]
             n += 1
     assert n >= 120
 
