@@ -331,6 +331,9 @@ __global__ void __launch_bounds__(kThreads) k_route_score(ScoreArgs a) {
   __shared__ PackedSeeds s_seeds[kWarpsPerBlock];
   __shared__ uint32_t s_tr[kWarpsPerBlock][32][33];
   __shared__ PatTable s_pat[kWarpsPerBlock];  // phase tables (truth words)
+  // the scan / compaction kernels may launch now and wait for this grid
+  // (programmatic dependent launch): their launch latency overlaps K1
+  asm volatile("griddepcontrol.launch_dependents;");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t task = blockIdx.x * kWarpsPerBlock + wid;
   if ((uint64_t)task >= (uint64_t)a.R * a.C) return;
@@ -775,6 +778,8 @@ __global__ void __launch_bounds__(1024)
                    uint64_t capacity, uint32_t* __restrict__ overflow) {
   extern __shared__ uint64_t s_t[];  // [kReqPer * 1024]
   __shared__ uint64_t warp_sums[32];
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's counts
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint64_t carry = 0;
   for (int t0 = 0; t0 < R; t0 += kReqPer * 1024) {
@@ -831,6 +836,25 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// Programmatic dependent launch: the kernel may begin while the previous
+// kernel on the stream still runs; it waits (griddepcontrol.wait) for that
+// grid's completion and memory before touching its outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+
 cudaError_t launch_request_scan(ag_ctx* ctx, cudaStream_t s, const uint64_t* counts, uint64_t* offsets, int R,
                                 uint64_t capacity, uint32_t* overflow) {
   bool& attr = ctx->scan_attr;
@@ -842,12 +866,10 @@ cudaError_t launch_request_scan(ag_ctx* ctx, cudaStream_t s, const uint64_t* cou
     attr = true;
   }
   if (R <= 4 * 1024)
-    k_request_scan<4><<<1, 1024, 4 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
-  else if (R <= 12 * 1024)
-    k_request_scan<12><<<1, 1024, 12 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
-  else
-    k_request_scan<24><<<1, 1024, 24 * 1024 * 8, s>>>(counts, offsets, R, capacity, overflow);
-  return cudaGetLastError();
+    return launch_pdl(k_request_scan<4>, 1, 1024, 4 * 1024 * 8, s, counts, offsets, R, capacity, overflow);
+  if (R <= 12 * 1024)
+    return launch_pdl(k_request_scan<12>, 1, 1024, 12 * 1024 * 8, s, counts, offsets, R, capacity, overflow);
+  return launch_pdl(k_request_scan<24>, 1, 1024, 24 * 1024 * 8, s, counts, offsets, R, capacity, overflow);
 }
 
 // K3: stream compaction of the verdict bitmap into canonical-order indices.
@@ -877,27 +899,49 @@ __global__ void __launch_bounds__(kThreads)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u, bit = 1u << lane;
   uint32_t* st = s_stage[wid];
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // K1's bitmap, K2's offsets
   const uint64_t units = (uint64_t)R * units_per_req;
   const uint32_t nwarps = gridDim.x * kWarpsPerBlock;
-  for (uint64_t unit = (uint64_t)blockIdx.x * kWarpsPerBlock + wid; unit < units; unit += nwarps) {
-    const uint32_t r = units_per_req == 1 ? (uint32_t)unit : (uint32_t)__umul64hi(unit, div_u);
-    const uint32_t u = (uint32_t)unit - r * units_per_req;
-    const uint32_t g0 = u * kUnitGroups;  // first group (32 words each)
+  // a unit's request and its output position; the next unit's are loaded
+  // while the current one is processed (two dependent global loads)
+  auto unit_of = [&](uint64_t unit, uint32_t& r, uint32_t& g0) {
+    r = units_per_req == 1 ? (uint32_t)unit : (uint32_t)__umul64hi(unit, div_u);
+    g0 = ((uint32_t)unit - r * units_per_req) * kUnitGroups;  // first group (32 words each)
+  };
+  uint64_t unit = (uint64_t)blockIdx.x * kWarpsPerBlock + wid;
+  uint64_t gs_next = 0;
+  if (unit < units) {
+    uint32_t r, g0;
+    unit_of(unit, r, g0);
+    gs_next = __ldg(offsets + r) + __ldg(group_off + (size_t)r * C * 32 + g0);
+  }
+  for (; unit < units; unit += nwarps) {
+    uint32_t r, g0;
+    unit_of(unit, r, g0);
     const uint32_t wbeg = g0 * 32;
     const uint32_t wend = min(W, wbeg + 32 * kUnitGroups);
     // global output position of the unit's first member
-    const uint64_t gs = __ldg(offsets + r) + __ldg(group_off + (size_t)r * C * 32 + g0);
+    const uint64_t gs = gs_next;
+    if (unit + nwarps < units) {
+      uint32_t r2, g2;
+      unit_of(unit + nwarps, r2, g2);
+      gs_next = __ldg(offsets + r2) + __ldg(group_off + (size_t)r2 * C * 32 + g2);
+    }
     const uint32_t* brow = bitmap + (size_t)r * W;
     const uint32_t phase0 = (uint32_t)(reinterpret_cast<uintptr_t>(indices + gs) >> 2) & 3u;
     uint32_t* gal = indices + (gs - phase0);  // 16-byte aligned output cursor (stage[0])
     uint64_t gpos = gs - phase0;              // its global index
     uint32_t fill = phase0;  // stage[0, fill): carried members (or, at first, not ours)
     uint32_t skip = phase0;  // leading stage entries that are not ours (first vector only)
+    // bitmap words two iterations ahead (empty iterations are short)
     uint32_t next = wbeg + lane < wend ? __ldg(brow + wbeg + lane) : 0u;
+    uint32_t next2 = wbeg + 32 + lane < wend ? __ldg(brow + wbeg + 32 + lane) : 0u;
+    uint32_t carry = 0;  // lanes < fill: the members carried into the next vector
     for (uint32_t wb = wbeg; wb < wend; wb += 32) {
       const uint32_t word = next;
-      const uint32_t wn = wb + 32 + lane;
-      next = wn < wend ? __ldg(brow + wn) : 0u;
+      next = next2;
+      const uint32_t wn = wb + 64 + lane;
+      next2 = wn < wend ? __ldg(brow + wn) : 0u;
       const uint32_t pc = __popc(word);
       uint32_t x = pc;
 #pragma unroll
@@ -907,6 +951,10 @@ __global__ void __launch_bounds__(kThreads)
       }
       const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
       if (total == 0) continue;
+      // the stage is rewritten: the previous bulk store must have read it
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      if (lane < fill) st[lane] = carry;
       s_word[wid][lane] = word;
       s_pre[wid][lane] = x - pc + fill;
       __syncwarp();
@@ -920,37 +968,41 @@ __global__ void __launch_bounds__(kThreads)
         if (ww.z & bit) st[pp.z + __popc(ww.z & lt)] = vl + 32u * (w4 + 2);
         if (ww.w & bit) st[pp.w + __popc(ww.w & lt)] = vl + 32u * (w4 + 3);
       }
+      // the staged members become visible to the bulk-copy (async) proxy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      // full vectors now; the partial last vector carries over
+      // full vectors now, as one bulk store (TMA engine: shared -> global,
+      // 16-byte aligned on both sides); the partial last vector carries over
       const uint32_t end = fill + total;
       const uint32_t nfull = end >> 2;
       const bool in_cap = gpos + 4ull * nfull <= capacity;
-      for (uint32_t v = lane; v < nfull; v += 32) {
-        const uint32_t e0 = 4 * v;
-        if (e0 >= skip && in_cap) {
-          *reinterpret_cast<uint4*>(gal + e0) = *reinterpret_cast<const uint4*>(st + e0);
-        } else {
-#pragma unroll
-          for (uint32_t q = 0; q < 4; ++q) {
-            const uint32_t e = e0 + q;
-            if (e >= skip && gpos + e < capacity) gal[e] = st[e];
-          }
+      const uint32_t v0 = skip ? 1u : 0u;  // a first vector holding entries not ours goes per lane
+      if (in_cap && nfull > v0) {
+        if (lane == 0) {
+          const uint32_t saddr = (uint32_t)__cvta_generic_to_shared(st + 4 * v0);
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n\t"
+                       "cp.async.bulk.commit_group;" ::"l"(gal + 4 * v0), "r"(saddr), "r"(16u * (nfull - v0))
+                       : "memory");
         }
+        if (v0 && lane < 4 && lane >= skip) gal[lane] = st[lane];
+      } else {
+        for (uint32_t e = lane; e < 4 * nfull; e += 32)
+          if (e >= skip && gpos + e < capacity) gal[e] = st[e];
       }
       const uint32_t tail = end & 3u;
-      const uint32_t t0 = lane < tail ? st[4 * nfull + lane] : 0u;
-      __syncwarp();
-      if (lane < tail) st[lane] = t0;
+      carry = lane < tail ? st[4 * nfull + lane] : 0u;
       if (nfull) skip = 0;
       fill = tail;
       gal += 4 * nfull;
       gpos += 4ull * nfull;
-      __syncwarp();
     }
     // the last partial vector
-    if (lane >= skip && lane < fill && gpos + lane < capacity) gal[lane] = st[lane];
+    if (lane >= skip && lane < fill && gpos + lane < capacity) gal[lane] = carry;
     __syncwarp();
   }
+  // every bulk store complete before the warp's stage goes away
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
 }
 
 template <int NT>
@@ -1074,9 +1126,8 @@ int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, c
   const uint64_t want = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)resident));
   Launch L(ctx, K_ROUTE_COMPACT);
-  k_route_compact<<<blocks, kThreads, 0, ctx->stream>>>(bitmap, (const uint64_t*)ctx->chunk_off.p, offsets,
-                                                        begin, W, C, upr, magic_div(upr), R, indices, capacity);
-  AG_CUDA(cudaGetLastError());
+  AG_CUDA(launch_pdl(k_route_compact, blocks, kThreads, 0, ctx->stream, bitmap, (const uint64_t*)ctx->chunk_off.p,
+                     offsets, begin, W, C, upr, magic_div(upr), R, indices, capacity));
   return AG_OK;
 }
 
