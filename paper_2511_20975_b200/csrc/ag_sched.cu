@@ -595,6 +595,90 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
         unsigned head = 0, have_l = 0;
         int jl = 0;
         bool exhausted = false;
+        // Head start: the first 64 FIFO positions straight from their pair
+        // records (the producers' first chunk takes several microseconds
+        // longer) -- the candidate records the producers will publish for
+        // them, in the same order, so the list is then followed from the
+        // number of candidates found here.  Only when every such position
+        // has at most one ready agent (chains; otherwise the producers' path).
+        {
+          constexpr int kHead = 64;
+          uint4 inf[2];
+          int npair[2], nq[2], nc[2];
+          bool multi = false;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int p = lane * 2 + i;
+            inf[i] = p < A.Q && p < kHead ? A.pinfo[p] : make_uint4(0u, 0u, 0u, 0u);
+            multi |= inf[i].w > 1u;
+            npair[i] = (int)inf[i].w;
+            nq[i] = inf[i].w ? 1 : 0;
+            nc[i] = inf[i].w == 1u && (inf[i].y & U0m) != 0u ? 1 : 0;
+          }
+          if (!__any_sync(kFull, multi)) {
+            // exclusive prefixes over positions: pairs, ready requests, candidates
+            int xp = npair[0] + npair[1], xq = nq[0] + nq[1], xc = nc[0] + nc[1];
+            int ip = xp, iq = xq, ic = xc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int a1 = __shfl_up_sync(kFull, ip, o), a2 = __shfl_up_sync(kFull, iq, o),
+                        a3 = __shfl_up_sync(kFull, ic, o);
+              if (lane >= o) ip += a1, iq += a2, ic += a3;
+            }
+            const int n_cand = __shfl_sync(kFull, ic, 31);
+            int bp = ip - xp, bq = iq - xq, bc = ic - xc;
+            const uint32_t U = *(volatile uint32_t*)&s_U;
+            // ring entries for the candidates meeting U, in order
+            int hits[2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const uint32_t em = nc[i] ? (s_emtab[0][inf[i].y & 255] | s_emtab[1][(inf[i].y >> 8) & 255] |
+                                           s_emtab[2][(inf[i].y >> 16) & 255] | s_emtab[3][inf[i].y >> 24]) & U0
+                                        : 0u;
+              hits[i] = (em & U) != 0u ? 1 : 0;
+              inf[i].y = em;
+            }
+            int xh = hits[0] + hits[1], ih = xh;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int a = __shfl_up_sync(kFull, ih, o);
+              if (lane >= o) ih += a;
+            }
+            const int n_hit = __shfl_sync(kFull, ih, 31);
+            int bh = ih - xh;
+            if (n_hit <= LA) {
+#pragma unroll
+              for (int i = 0; i < 2; ++i) {
+                const int p = lane * 2 + i;
+                if (hits[i]) {
+                  const int sl = bh & (LA - 1);
+                  s_la_rec[sl] = Cand{(uint32_t)bp, A.cidx ? A.cidx[p] : bq, inf[i].x, inf[i].z};
+                  s_la_mask[sl] = inf[i].y;
+                  ++bh;
+                }
+                bp += npair[i];
+                bq += nq[i];
+                bc += nc[i];
+              }
+              __syncwarp();
+              for (int e = lane; e < n_hit * M; e += 32) {
+                const int k = e / M, mdl = e - k * M;
+                const Cand r = s_la_rec[k];
+                const int a = (int)(r.slot_agent >> 26), slt = (int)(r.slot_agent & 0x3ffffffu);
+                const uint32_t sv = __ldg(A.hist + ((size_t)slt * N + a) * M + mdl);
+                h_cnt[k * M + mdl] = sv;
+                h_rat[k * M + mdl] = (double)sv / (double)r.nvia;
+              }
+              __syncwarp();
+              if (lane == 0 && n_hit) {
+                __threadfence_block();
+                st_release(&s_la_head, (unsigned)n_hit);
+              }
+              head = (unsigned)n_hit;
+              jl = n_cand;  // the producers' candidates of these positions are covered
+            }
+          }
+        }
         while (!exhausted) {
           // room in the ring (entries below the walker's tail are consumed)
           unsigned tail = 0;
