@@ -59,6 +59,8 @@ struct CostArgs {
   uint64_t* tsize;              // members per task (k_cost_plan)
   int32_t* t_req;               // [tasks] request of each task (k_cost_plan)
   uint64_t* rec;                // [R][4] shard records (ag_shard_records) or null
+  uint32_t m_magic;             // ceil(2^32 / M): exact x / M for x < 2^32 / M (suffix digits)
+  int any_missing;              // some tier's estimate term is NaN (a missing tier)
   int allow_empty;              // shard records: an empty shard is not an error
   uint32_t* chosen;
   double* est;
@@ -144,16 +146,19 @@ __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ Cost
 // M^N <= 2^32 and M^k <= kPrefixMax leave at most 16).
 template <int SFX>
 __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_constant__ CostArgs A) {
-  __shared__ double s_term[kMaxModels + 1], s_cost[kMaxModels + 1];
+  // per tier: (estimate term, static cost), one 16-byte load per digit
+  __shared__ double2 s_tc[kMaxModels + 1];
   const int m_ = A.sp.m;
-  for (int i = threadIdx.x; i < m_; i += blockDim.x) {
-    s_term[i] = A.term[i];
-    s_cost[i] = A.cost[i];
-  }
+  for (int i = threadIdx.x; i < m_; i += blockDim.x) s_tc[i] = make_double2(A.term[i], A.cost[i]);
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int n_tasks = A.r_task[A.R];
   const uint64_t ts = *A.tsize;
+  const int sfx = SFX > 0 ? SFX : A.sp.n - A.k;
+  const uint32_t m = (uint32_t)m_, mk = A.mk, mg = A.m_magic;
+  const uint64_t div_mk = A.div_mk;
+  const double2* __restrict__ prefix = A.prefix;
+  const bool runtime = A.kind != 0, check_nan = A.any_missing != 0;
   // persistent warps over the tasks (their number is only known on the device)
   for (int t = blockIdx.x * kCostWarps + (threadIdx.x >> 5); t < n_tasks; t += gridDim.x * kCostWarps) {
   const int r = A.t_req[t];  // the task's request
@@ -161,11 +166,6 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_con
   const uint64_t rest = A.offsets[r + 1] - b0;
   const uint32_t len = (uint32_t)(rest < ts ? rest : ts);
   const uint32_t* mem = A.members + b0;
-  const int sfx = SFX > 0 ? SFX : A.sp.n - A.k;
-  const uint32_t m = (uint32_t)m_, mk = A.mk;
-  const uint64_t div_m = A.sp.div_m, div_mk = A.div_mk;
-  const double2* __restrict__ prefix = A.prefix;
-  const bool runtime = A.kind != 0;
   double be = INFINITY, bc = INFINITY;
   uint32_t bi = 0xffffffffu;
   bool missing = false;
@@ -184,25 +184,27 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_con
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       if (j + 32 * u >= len) break;
-      // suffix digits, last first, packed one per byte (two words: <= 16)
+      // suffix digits, last first: x < mk <= 2^32 / M, so x / M is one
+      // 32-bit high multiply (mg = ceil(2^32 / M) is exact below 2^32 / M)
       uint32_t x = idx[u] - q[u] * mk;
-      uint64_t pk[2] = {0, 0};
+      uint32_t d[SFX > 0 ? SFX : 16];
 #pragma unroll
       for (int a = (SFX > 0 ? SFX : 16) - 1; a >= 0; --a) {
         if (SFX == 0 && a >= sfx) continue;
-        const uint32_t qq = a > 0 ? divm(x, div_m) : 0u;
-        pk[a >> 3] |= (uint64_t)(x - qq * m) << (8 * (a & 7));
+        const uint32_t qq = a > 0 ? __umulhi(x, mg) : 0u;
+        d[a] = x - qq * m;
         x = qq;
       }
+      // the folds continue from the prefix, agent order, no contraction
       double e = pre[u].x, c = pre[u].y;
 #pragma unroll
       for (int a = 0; a < (SFX > 0 ? SFX : 16); ++a) {
         if (SFX == 0 && a >= sfx) break;
-        const uint32_t dg = (uint32_t)(pk[a >> 3] >> (8 * (a & 7))) & 0xFFu;
-        e += s_term[dg];
-        c += s_cost[dg];
+        const double2 tc = s_tc[d[a]];
+        e = __dadd_rn(e, tc.x);
+        c = __dadd_rn(c, tc.y);
       }
-      missing |= isnan(e);  // a NaN term (missing tier) anywhere in the fold
+      if (check_nan) missing |= isnan(e);  // a NaN term (missing tier) anywhere in the fold
       if (!runtime) e = 0.0;
       if (key_less(e, c, idx[u], be, bc, bi)) be = e, bc = c, bi = idx[u];
     }
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_con
     const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (key_less(oe, oc, oi, be, bc, bi)) be = oe, bc = oc, bi = oi;
   }
-  if (__any_sync(0xffffffffu, missing) && lane == 0) atomicOr(A.status, 1);
+  if (check_nan && __any_sync(0xffffffffu, missing) && lane == 0) atomicOr(A.status, 1);
   if (lane == 0) A.task_best[t] = Key{be, bc, bi};
   }
 }
@@ -311,12 +313,15 @@ int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, i
     A.term[i] = 0.0;
     A.cost[i] = i < sp->m ? sp->cost[i] : 0.0;
   }
+  A.m_magic = (uint32_t)((0x100000000ull + (uint64_t)sp->m - 1) / (uint64_t)sp->m);
+  A.any_missing = 0;
   if (A.kind == 1) {
     // estimate_completion (workload.cpp:129-147)
     if (load->n_tiers < 0) return fail(AG_ERR_VALIDATION, "estimator context arrays disagree on tier count");
     for (int i = 0; i < sp->m; ++i) {
       if (i >= load->n_tiers || load->slots[i] <= 0) {
         A.term[i] = NAN;  // an error only if a member uses the tier
+        A.any_missing = 1;
         continue;
       }
       const double ld = (double)(load->occupancy[i] + load->queued_ahead[i]);
@@ -371,14 +376,20 @@ int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, i
   }
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    if (!ctx->cost_grid) {
+    // grid = the resident capacity of the variant launched (occupancy differs
+    // by suffix length: the generic variant keeps 16 digits in registers)
+    const int sfx = sp->n - A.k;
+    const int vi = sfx >= 1 && sfx <= 4 ? sfx : 0;
+    if (!ctx->cost_grid[vi]) {
+      static void (*const fns[5])(agb::CostArgs) = {agb::k_cost_tasks<0>, agb::k_cost_tasks<1>, agb::k_cost_tasks<2>,
+                                                   agb::k_cost_tasks<3>, agb::k_cost_tasks<4>};
       int sms = 0, per_sm = 0;
       AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-      AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, agb::k_cost_tasks<0>, agb::kCostWarps * 32, 0));
-      ctx->cost_grid = std::max(1, sms * per_sm);
+      AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[vi], agb::kCostWarps * 32, 0));
+      ctx->cost_grid[vi] = std::max(1, sms * per_sm);
     }
-    const dim3 g(ctx->cost_grid), b(agb::kCostWarps * 32);
-    switch (sp->n - A.k) {
+    const dim3 g(ctx->cost_grid[vi]), b(agb::kCostWarps * 32);
+    switch (vi) {
       case 1: agb::k_cost_tasks<1><<<g, b, 0, st>>>(A); break;
       case 2: agb::k_cost_tasks<2><<<g, b, 0, st>>>(A); break;
       case 3: agb::k_cost_tasks<3><<<g, b, 0, st>>>(A); break;

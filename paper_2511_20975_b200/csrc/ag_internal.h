@@ -83,7 +83,7 @@ struct ag_ctx {
   agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
   bool hc_ready = false;
   agb::Scratch cost_status, cost_tasks, cost_prefix;  // runtime-cost argmin: plan, task bests, prefix folds
-  int cost_grid = 0;                                  // k_cost_tasks blocks resident on the device
+  int cost_grid[5] = {0, 0, 0, 0, 0};                 // k_cost_tasks<sfx> blocks resident on the device
   int colmask_m = 0;
   // host-path staging
   agb::Scratch h_truth;
