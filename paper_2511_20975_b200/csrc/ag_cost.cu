@@ -32,7 +32,8 @@ namespace agb {
 namespace {
 
 constexpr int kCostWarps = 8;
-constexpr uint64_t kTask = 1 << 16;     // members per task (at least)
+constexpr uint64_t kTask = 1 << 13;     // members per task (at least; a power of two)
+constexpr int kPlanSmemReq = 24 * 1024;  // requests whose offsets the plan stages in shared memory
 constexpr uint64_t kTaskCap = 1 << 20;  // tasks per call beyond one per request
 constexpr uint64_t kPrefixMax = 1u << 22;  // prefix-table entries (64 MB)
 
@@ -99,19 +100,28 @@ __global__ void __launch_bounds__(256) k_cost_prefix(const __grid_constant__ Cos
 // gets no task.
 __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ CostArgs A) {
   __shared__ int32_t s_wsum[32];
+  extern __shared__ uint64_t s_off[];  // [R+1] when R < kPlanSmemReq
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const uint64_t total = A.offsets[A.R] - A.offsets[0];
+  const bool staged = A.R < kPlanSmemReq;
+  if (staged)
+    for (int i = tid; i <= A.R; i += 1024) s_off[i] = A.offsets[i];  // coalesced
+  __syncthreads();
+  auto off = [&](int i) -> uint64_t { return staged ? s_off[i] : A.offsets[i]; };
+  // tasks of ts members, ts a power of two >= total / kTaskCap
+  const uint64_t total = off(A.R) - off(0);
   const uint64_t tq = (total + kTaskCap - 1) / kTaskCap;
-  const uint64_t ts = tq > kTask ? tq : kTask;
+  uint64_t ts = kTask;
+  while (ts < tq) ts <<= 1;
+  const int sh = __ffsll((long long)ts) - 1;
   if (tid == 0) *A.tsize = ts;
   // thread tid plans the contiguous requests [r0, r1): one pass, one scan
   const int per = (A.R + 1023) / 1024;
   const int r0 = min(A.R, tid * per), r1 = min(A.R, r0 + per);
   int32_t mine = 0;
   for (int r = r0; r < r1; ++r) {
-    const uint64_t len = A.offsets[r + 1] - A.offsets[r];
+    const uint64_t len = off(r + 1) - off(r);
     if (len == 0 && !A.allow_empty) atomicOr(A.status, 2);
-    mine += (int32_t)((len + ts - 1) / ts);
+    mine += (int32_t)((len + ts - 1) >> sh);
   }
   int32_t x = mine;
 #pragma unroll
@@ -136,7 +146,7 @@ __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ Cost
   int32_t acc = s_wsum[w] + x - mine;
   for (int r = r0; r < r1; ++r) {
     A.r_task[r] = acc;
-    const int32_t nt = (int32_t)((A.offsets[r + 1] - A.offsets[r] + ts - 1) / ts);
+    const int32_t nt = (int32_t)((off(r + 1) - off(r) + ts - 1) >> sh);
     for (int32_t k = 0; k < nt; ++k) A.t_req[acc + k] = r;
     acc += nt;
   }
@@ -222,12 +232,17 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_tasks(const __grid_con
 }
 
 __global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const __grid_constant__ CostArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int r = blockIdx.x * kCostWarps + (threadIdx.x >> 5);
-  if (r >= A.R) return;
+  // few requests (deep spaces: thousands of tasks each): one block per
+  // request and a block reduction; many requests: one warp per request
+  __shared__ Key s_k[kCostWarps];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool per_block = A.R <= 1024;
+  const int r = per_block ? (int)blockIdx.x : (int)blockIdx.x * kCostWarps + wid;
+  if (!per_block && r >= A.R) return;
   double be = INFINITY, bc = INFINITY;
   uint32_t bi = 0xffffffffu;
-  for (int t = A.r_task[r] + lane; t < A.r_task[r + 1]; t += 32) {
+  const int t0 = A.r_task[r] + (per_block ? (int)threadIdx.x : lane), dt = per_block ? kCostWarps * 32 : 32;
+  for (int t = t0; t < A.r_task[r + 1]; t += dt) {
     const Key k = A.task_best[t];
     if (key_less(k.e, k.c, k.i, be, bc, bi)) be = k.e, bc = k.c, bi = k.i;
   }
@@ -237,6 +252,24 @@ __global__ void __launch_bounds__(kCostWarps * 32) k_cost_reduce(const __grid_co
     const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
     const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (key_less(oe, oc, oi, be, bc, bi)) be = oe, bc = oc, bi = oi;
+  }
+  if (per_block) {
+    if (lane == 0) s_k[wid] = Key{be, bc, bi};
+    __syncthreads();
+    if (wid != 0) return;
+    if (lane < kCostWarps) {
+      const Key k = s_k[lane];
+      be = k.e, bc = k.c, bi = k.i;
+    } else {
+      be = INFINITY, bc = INFINITY, bi = 0xffffffffu;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double oe = __shfl_xor_sync(0xffffffffu, be, o);
+      const double oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const uint32_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (key_less(oe, oc, oi, be, bc, bi)) be = oe, bc = oc, bi = oi;
+    }
   }
   if (lane == 0) {
     if (A.chosen) A.chosen[r] = bi;
@@ -368,7 +401,13 @@ int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, i
   A.task_best = (agb::Key*)ctx->cost_tasks.p;
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    agb::k_cost_plan<<<1, 1024, 0, st>>>(A);
+    const size_t psm = R < agb::kPlanSmemReq ? 8 * ((size_t)R + 1) : 0;
+    if (psm > 48 * 1024 && !ctx->cost_plan_attr) {
+      AG_CUDA(cudaFuncSetAttribute(agb::k_cost_plan, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   8 * agb::kPlanSmemReq));
+      ctx->cost_plan_attr = true;
+    }
+    agb::k_cost_plan<<<1, 1024, psm, st>>>(A);
   }
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
@@ -399,7 +438,8 @@ int select_impl(ag_ctx* ctx, const uint32_t* members, const uint64_t* offsets, i
   }
   {
     agb::Launch L(ctx, agb::K_COST_ARGMIN);
-    agb::k_cost_reduce<<<(R + agb::kCostWarps - 1) / agb::kCostWarps, agb::kCostWarps * 32, 0, st>>>(A);
+    const unsigned rb = R <= 1024 ? (unsigned)R : (unsigned)((R + agb::kCostWarps - 1) / agb::kCostWarps);
+    agb::k_cost_reduce<<<rb, agb::kCostWarps * 32, 0, st>>>(A);
   }
   AG_CUDA(cudaGetLastError());
   return AG_OK;

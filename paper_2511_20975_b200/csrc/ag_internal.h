@@ -84,6 +84,7 @@ struct ag_ctx {
   bool hc_ready = false;
   agb::Scratch cost_status, cost_tasks, cost_prefix;  // runtime-cost argmin: plan, task bests, prefix folds
   int cost_grid[5] = {0, 0, 0, 0, 0};                 // k_cost_tasks<sfx> blocks resident on the device
+  bool cost_plan_attr = false;                        // k_cost_plan's dynamic shared memory raised
   int colmask_m = 0;
   // host-path staging
   agb::Scratch h_truth;
