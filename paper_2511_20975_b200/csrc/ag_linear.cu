@@ -102,10 +102,6 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* mb, uint32_t parity) {
     __nanosleep(32);
   }
 }
-__device__ __forceinline__ void umma_commit(uint64_t* mb) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(mb))
-               : "memory");
-}
 __device__ __forceinline__ void umma_commit_elect(uint64_t* mb) {
   asm volatile(
       "{ .reg .pred e; elect.sync _|e, 0xffffffff;\n"

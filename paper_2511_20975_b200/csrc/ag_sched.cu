@@ -38,13 +38,25 @@
 //     soon as every branch is full or the candidates are exhausted; the
 //     queue's pair count comes from the host mirror, so the producers stop
 //     scanning once the walker is done (unless validation needs every pair);
+//   * the fast walker (B <= 4, <= 8 pools; ag_sched_fast.cuh) is fed by a
+//     lookahead warp (warp 1) instead: it reads the first 64 positions' pair
+//     records itself (a head start before the producers' first chunk), then
+//     follows the producers' list, and hands the walker the candidates that
+//     meet its current free-engine union through a 64-entry shared-memory
+//     ring together with their histogram rows -- the walker's steps read
+//     shared memory only;
 //   * finalize: the winner's triples from the tree (written in parallel),
 //     score_assignment's utilization and flexibility folded in the
 //     reference's order;
 //   * the round's input deltas (ready masks, FIFO tail) are read by the
 //     kernel from mapped pinned host memory and the assignment is written
-//     straight back into it: one launch and one stream synchronisation per
-//     round, no separate copies.
+//     straight back into it: one launch per round, the host spinning on the
+//     round's sequence number in the mapped result.  Large record batches
+//     (a FIFO compaction, an arrival batch) are applied when they happen by
+//     k_sched_refresh, outside the decision.
+// Also here: k_sched_prune (mark_dispatched's prefix prune + histograms),
+// k_sched_audit (audit_round_fairness, scheduler.cpp:456-480), the viable
+// pool compaction (k_pool_scan / k_pool_copy) and k_queued_ahead.
 // All fp64 arithmetic repeats the reference's operations in the same order
 // (the library builds with --fmad=false).
 #include <cuda_runtime.h>
@@ -97,7 +109,6 @@ struct RoundShape {
   static constexpr int producers = threads / 4 * 3 - (BM > 0 ? 32 : 0);
 };
 constexpr int kLookahead = 64;  // lookahead ring entries (a power of two)
-constexpr int kMaxRoundThreads = 512;
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
 constexpr int kSmemNodes = 1024;
@@ -290,9 +301,6 @@ __device__ __forceinline__ uint64_t rel_extend_sel(bool same, uint64_t r12, uint
   return same ? s_res : o_res;
 }
 
-// surv / initial for a histogram row the producers have not staged: out of
-// line, so the division is not if-converted into the walker's common path
-__device__ __noinline__ double ratio_slow(uint32_t surv, double initial) { return (double)surv / initial; }
 
 // order-preserving u64 image of an f64 (no NaNs here; -0 == +0)
 __device__ __forceinline__ uint64_t okey(double d) {
