@@ -142,3 +142,25 @@ def test_config4_full_space_matches_reference_digest():
             torch.cuda.empty_cache()
         assert [tuple(x) for x in acc] == whole, G
         assert _digest_of(acc) == ref["digest"], G
+
+
+def test_config4_noisy_full_space_matches_reference_digest():
+    """Config 4 (8 x 12, 16 requests, 6.9e9 verdicts) with the noisy router of
+    config 2 (fp 0, fn 0.3, seed 7): a space above the 2^24 hash-table limit,
+    so every verdict takes the per-word hash-chain path of k_route_noise
+    (router.cpp:50-57, rng.h:34-51) -- the checksum of per-request
+    (count, sum, sum of squares) against the unmodified reference loop."""
+    if not os.path.exists(REF):
+        pytest.skip("oracle/_ref/ref_bench not built")
+    n, m, R4 = 8, 12, 16
+    out = subprocess.run([REF, "route", str(n), str(m), str(R4), "noisy", str(os.cpu_count() or 1), str(SEED)],
+                         capture_output=True, text=True, check=True, timeout=1800).stdout
+    ref = json.loads(out.strip().splitlines()[-1])
+    space = P.ConfigSpace.chain(n, m)
+    dev = P.Device(space)
+    truth = P.AccuracyBatch.generate(space, P.GenParams(), R4, SEED).to_device()
+    res = dev.route_enumerate(truth, P.NoisyRouter(0.0, 0.3, 7))
+    torch.cuda.synchronize()
+    rows = _sums_dev(res, R4)
+    assert sum(c for c, _, _ in rows) == ref["members"]
+    assert _digest_of(rows) == ref["digest"]
