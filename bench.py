@@ -67,6 +67,10 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # multi-rank logic check on a one-GPU box (tests only): every rank on
+    # cuda:0, gloo for the collectives (NCCL refuses two ranks on one device)
+    if os.environ.get("AG_BENCH_ONE_DEVICE") == "1":
+        local = 0
     return ws, rank, local
 
 
@@ -587,7 +591,10 @@ def run_ours(args):
     if ws > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("AG_BENCH_ONE_DEVICE") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev_t = torch.device("cuda", local)
     clocks = Clocks(local)
