@@ -406,14 +406,14 @@ bool resident_round(Gpu& g, const std::vector<const Request*>& queue, int M, con
   Resident& R = *g.res;
   std::uint64_t need = 0;
   for (const Request* r : queue) need += r->viable.size();
-  if (!R.s || (int)queue.size() * 2 > R.cap || need * 4 > R.pool) {
+  if (!R.s || (int)queue.size() * 2 > R.cap || need * 2 > R.pool) {
     // (re)create, sized with headroom; everything is re-added below
     if (R.s) ag_sched_destroy(R.s);
     R.s = nullptr;
     R.live.clear();
     R.last.clear();
     R.cap = std::max(1024, 4 * (int)queue.size());
-    R.pool = std::max<std::uint64_t>(1u << 20, 16 * need);
+    R.pool = std::max<std::uint64_t>(1u << 20, 4 * need);  // a capacity: packed on the device when full
     if (ag_sched_create(g.ctx, R.cap, R.pool, &R.s) != AG_OK) {
       R.s = nullptr;
       return false;

@@ -56,8 +56,12 @@ extern "C" int ag_trace_write(ag_ctx* ctx, const ag_truth* th, const double* arr
     t.removed_ptr = th->removed_ptr + r0;
     counts.assign(n, 0);
     offsets.assign((size_t)n + 1, 0);
-    idx.assign((size_t)n * S + 1, 0);
+    // the chunk's member total first (counts only), then exactly that much
+    // host memory for the indices
     uint64_t total = 0;
+    rc = ag_route_enumerate_host(ctx, &t, &oracle, 0, S, 0, counts.data(), offsets.data(), nullptr, 0, &total);
+    if (rc) break;
+    idx.assign((size_t)total + 1, 0);
     rc = ag_route_enumerate_host(ctx, &t, &oracle, 0, S, 0, counts.data(), offsets.data(), idx.data(), idx.size(),
                                  &total);
     if (rc) break;
