@@ -353,7 +353,8 @@ def run_sched(P, W, dev, args, rounds=None, beam=SCHED_BEAM, exhaustive=False):
                     "assignment download); device = the round kernel alone"}
 
 
-def run_select(P, dev, sets, members, offsets, n_members, stream, flush, barrier, with_ref):
+def run_select(P, dev, sets, members, offsets, n_members, stream, flush, barrier, with_ref, bitmap=None,
+               counts=None):
     """The per-stage re-cost + argmin of config 3:
     select_per_input_config(set, space, kPerInputRuntimeCost, &ctx) for all
     10k requests of the batch, device-resident member CSR, CUDA-event timed
@@ -393,6 +394,33 @@ def run_select(P, dev, sets, members, offsets, n_members, stream, flush, barrier
                         "achieved": 4.0 * n_members / (kms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
                         "frac": 4.0 * n_members / (kms / 1e3) / 1e9 / hbm, "peak_source": psrc,
                         "algorithmic_bytes_per_launch": 4 * n_members}}
+    if bitmap is not None:
+        # the same selection straight from the verdict bitmap (ag_select_bitmap)
+        S = dev.space.size
+        for _ in range(3):
+            bch, best = P.select_bitmap(dev, bitmap, counts, 0, S, P.PER_INPUT_RUNTIME_COST, load,
+                                        check_errors=False)
+        dev.synchronize()
+        barrier()
+        dev.profile_begin()
+        for i in range(10):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            bch, best = P.select_bitmap(dev, bitmap, counts, 0, S, P.PER_INPUT_RUNTIME_COST, load,
+                                        check_errors=False)
+            ev[i][1].record(stream)
+        bprof = dev.profile_end()
+        dev.synchronize()
+        bms = statistics.median([a.elapsed_time(b) for a, b in ev])
+        bkms = bprof["k_cost_argmin"][0] / 10 if "k_cost_argmin" in bprof else bms
+        bbytes = R * ((S + 31) // 32) * 4
+        out["bitmap_path"] = {
+            "us_per_batch": bms * 1e3, "configs_costed_per_s": n_members / (bms / 1e3), "launches_per_batch": 3,
+            "same_as_member_path": bool(torch.equal(bch, ch) and torch.equal(best, est)),
+            "roofline": {"bound": "hbm", "kernel": "k_bm_prefix/eval/reduce",
+                         "achieved": bbytes / (bkms / 1e3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": bbytes / (bkms / 1e3) / 1e9 / hbm, "peak_source": psrc,
+                         "algorithmic_bytes_per_launch": bbytes}}
     if with_ref and os.path.exists(REF_BENCH):
         n = SELECT_CPU_SAMPLE[sets]
         ref = ref_select(sets, n, os.cpu_count())
@@ -425,7 +453,7 @@ def run_deep(P, args, ws, rank, local, barrier):
     probe = dev.route_enumerate(truth, router, begin, end, compact=False)
     torch.cuda.synchronize()
     cap = int(probe.offsets[-1])
-    out = dev.alloc_route(R, begin, end, cap)
+    out = dev.alloc_route(R, begin, end, cap, bitmap=True)  # the argmin reads the verdict bitmap
     mean = [0.05 + float(np.exp(-0.3 + 0.35 * i + 0.5 * 0.25 * 0.25)) for i in range(m)]
     load = P.RuntimeCostContext([4] * m, [i % 3 for i in range(m)], [8] * m, mean)
     times = []
@@ -456,7 +484,7 @@ def run_deep(P, args, ws, rank, local, barrier):
     torch.cuda.empty_cache()
     return {"workload": "config4: chain 8 x 12 tiers (4.3e8 configs/request), 16 requests, "
                         f"canonical-index space sharded over {ws} GPU(s), oracle router, "
-                        "enumerate + compact + runtime-cost argmin + all-gather of 32-byte "
+                        "enumerate + compact + runtime-cost argmin from the verdict bitmap + all-gather of 32-byte "
                         "per-shard records",
             "configs_per_s": configs / dt, "ms_per_step": dt * 1e3, "scaling": "strong",
             "members": int(total.sum()), "n_gpus": ws,
@@ -611,7 +639,7 @@ def run_ours(args):
     probe = dev.route_enumerate(truth, router, compact=False)
     torch.cuda.synchronize()
     total_members = int(probe.offsets[-1])
-    out = dev.alloc_route(REQUESTS_PER_GPU, 0, S, total_members)
+    out = dev.alloc_route(REQUESTS_PER_GPU, 0, S, total_members, bitmap=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev_t)
 
     def step():
@@ -731,7 +759,8 @@ def run_ours(args):
     select = None
     if not args.no_select:
         select = run_select(P, dev, "exhaustive", out["indices"], out["offsets"], total_members, stream,
-                            flush, barrier, rank == 0 and not args.no_cpu_baseline)
+                            flush, barrier, rank == 0 and not args.no_cpu_baseline, out["bitmap"],
+                            out["counts"])
         if chain and csel:
             select["viable_sets"] = csel
     # the learned router: per-configuration linear
@@ -921,6 +950,7 @@ def summarize(line, sched, deep, noisy, linear, chain, config5, select=None, con
         out["chain_requests_per_s"] = _r(chain["requests_per_s"])
     if select:
         out["select_us"] = {"exhaustive": _r(select["us_per_batch"]),
+                            "bitmap": _r((select.get("bitmap_path") or {}).get("us_per_batch")),
                             "frac": _r(select["roofline"]["frac"]),
                             "ref": _r((select.get("reference") or {}).get("us_per_batch")),
                             "match": select.get("digest_match")}

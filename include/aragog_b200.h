@@ -382,6 +382,24 @@ int ag_select_per_input(ag_ctx* ctx, const uint32_t* members,
                         int32_t kind, const ag_load* load, uint32_t* chosen,
                         double* est);
 
+/* The same selection straight from enumerate mode's verdict bitmap
+ * (ag_route_out.bitmap over [begin, end), counts [R]) -- no member list:
+ * prefix lower bounds of the key's primary term (estimate; static cost for
+ * the static kind) prune the words that cannot hold the minimum, the rest
+ * are re-costed exactly, so chosen / est equal ag_select_per_input's on the
+ * same set (indices are canonical: begin + position).  records [R][4]
+ * optional, as ag_shard_records (an empty shard is not an error there);
+ * chosen may be NULL when records is set.  Asynchronous; errors latch as
+ * ag_select_per_input's.  Replaces the same call sites. */
+int ag_select_bitmap(ag_ctx* ctx, const uint32_t* bitmap, const uint64_t* counts,
+                     uint64_t begin, uint64_t end, int32_t n_requests, int32_t kind,
+                     const ag_load* load, uint32_t* chosen, double* est,
+                     uint64_t* records);
+/* Diagnostics: enable = 1 starts counting the words ag_select_bitmap's
+ * exact pass evaluates on this context; enable = 0 stops and returns the
+ * count (synchronises the context stream). */
+int ag_select_bitmap_stats(ag_ctx* ctx, int32_t enable, uint64_t* words_evaluated);
+
 /* ---- configuration-space sharding (config 4) ---------- */
 /* Per-shard record of select_per_input_config over this rank's canonical
  * index range: records [R][4] u64 (device) = {member count, estimate (f64

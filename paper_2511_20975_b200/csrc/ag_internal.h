@@ -83,6 +83,9 @@ struct ag_ctx {
   agb::Scratch hc;       // hash_config(c) per canonical index (noisy router)
   bool hc_ready = false;
   agb::Scratch cost_status, cost_tasks, cost_prefix;  // runtime-cost argmin: plan, task bests, prefix folds
+  agb::Scratch cost_bm;                                // bitmap argmin: prefix lower bounds + thresholds
+  agb::Scratch bm_stats;                               // bitmap argmin diagnostics: words evaluated
+  bool bm_stats_on = false;
   int cost_grid[5] = {0, 0, 0, 0, 0};                 // k_cost_tasks<sfx> blocks resident on the device
   bool cost_plan_attr = false;                        // k_cost_plan's dynamic shared memory raised
   int colmask_m = 0;

@@ -100,10 +100,12 @@ def exchange_records(rec, world: int, group=None):
     return out.view((world,) + tuple(rec.shape))
 
 
-def shard_records(dev, res, n_requests: int, load_ctx=None):
+def shard_records(dev, res, n_requests: int, load_ctx=None, begin=None, end=None):
     """The [R, 4] int64 device records of this shard (ag_shard_records):
     {count, estimate bits, static-cost bits, index} of the runtime-cost
-    minimum, or counts only without a load context."""
+    minimum, or counts only without a load context.  When the routing result
+    carries its verdict bitmap and the shard range is given, the records come
+    straight from the bitmap (ag_select_bitmap: no member-list read)."""
     import ctypes as C
 
     import torch
@@ -115,6 +117,12 @@ def shard_records(dev, res, n_requests: int, load_ctx=None):
     rec = torch.zeros((max(n_requests, 1), REC_WORDS), dtype=torch.int64, device=dev.torch_device)
     if load_ctx is None:
         rec[:n_requests, 0] = res.counts[:n_requests].to(torch.int64)
+        return rec[:n_requests]
+    if res.bitmap is not None and begin is not None:
+        from .scheduler import select_bitmap
+
+        select_bitmap(dev, res.bitmap, res.counts[:n_requests], begin, end, PER_INPUT_RUNTIME_COST, load_ctx,
+                      check_errors=False, records=rec)
         return rec[:n_requests]
     load = load_ctx.c()
     check(lib().ag_shard_records(dev.handle, C.c_void_p(_ptr(res.indices)), C.c_void_p(_ptr(res.offsets)),
@@ -148,7 +156,8 @@ def merge_device(dev, gathered, rank: int):
 def route_space_sharded(dev, truth_dev, router, rank, world, load_ctx=None, out=None, group=None):
     """Config 4: every rank enumerates its canonical-index shard of every
     request (ag_route_enumerate over [begin, end)), reduces it to one 32-byte
-    record per request on the device (ag_shard_records), then ONE all-gather
+    record per request on the device (ag_select_bitmap from the verdict
+    bitmap when `out` holds one, else ag_shard_records), then ONE all-gather
     of the records and a device-side merge (ag_merge_records).  No host
     round trip anywhere: everything is enqueued on the device's stream.
     Returns the local result, the global counts, this shard's global offsets
@@ -157,7 +166,7 @@ def route_space_sharded(dev, truth_dev, router, rank, world, load_ctx=None, out=
     begin, end = shard_range(dev.space.size, rank, world)
     res = dev.route_enumerate(truth_dev, router, begin, end, out=out)
     R = truth_dev.n_requests
-    rec = shard_records(dev, res, R, load_ctx)
+    rec = shard_records(dev, res, R, load_ctx, begin, end)
     gathered = exchange_records(rec, world, group)
     total, before, best = merge_device(dev, gathered, rank)
     return res, total, before, best

@@ -287,6 +287,37 @@ def select_per_input(device: Device, members, offsets, kind=PER_INPUT_RUNTIME_CO
     return chosen[:R], est[:R]
 
 
+def select_bitmap(device: Device, bitmap, counts, begin: int, end: int, kind=PER_INPUT_RUNTIME_COST, ctx=None,
+                  check_errors=True, records=None):
+    """select_per_input_config straight from an enumerate-mode verdict bitmap
+    (device tensors: bitmap int32 [R, W] over [begin, end), counts int64 [R])
+    -- ag_select_bitmap: the same (chosen canonical index, estimate) as
+    select_per_input over the compacted members, without the member list.
+    records: optional int64 [R, 4] device tensor receiving the shard records
+    (ag_shard_records' layout; empty sets allowed then)."""
+    import torch
+
+    R = counts.numel()
+    chosen = torch.zeros(max(R, 1), dtype=torch.int32, device=device.torch_device)
+    est = torch.zeros(max(R, 1), dtype=torch.float64, device=device.torch_device)
+    load = ctx.c() if ctx is not None else None
+    check(lib().ag_select_bitmap(device.handle, C.c_void_p(_ptr(bitmap)), C.c_void_p(_ptr(counts)),
+                                 C.c_uint64(begin), C.c_uint64(end), R, kind,
+                                 C.byref(load) if load is not None else None, C.c_void_p(_ptr(chosen)),
+                                 C.c_void_p(_ptr(est)), C.c_void_p(_ptr(records) if records is not None else None)))
+    if check_errors:
+        check(lib().ag_ctx_synchronize(device.handle))
+    return chosen[:R], est[:R]
+
+
+def select_bitmap_stats(device: Device, enable: bool) -> int:
+    """ag_select_bitmap_stats: start (enable) or stop counting the words the
+    exact pass of select_bitmap evaluates; returns the count on stop."""
+    out = C.c_uint64()
+    check(lib().ag_select_bitmap_stats(device.handle, 1 if enable else 0, C.byref(out)))
+    return int(out.value)
+
+
 def select_per_workflow(device: Device, sample, tolerance: float = 0.0):
     """select_per_workflow_config(sample, space, tolerance) (workload.cpp:99-127)
     over a host AccuracyBatch, without the 4096-configuration guard: returns
