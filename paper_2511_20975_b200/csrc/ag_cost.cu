@@ -336,7 +336,10 @@ constexpr uint32_t kBmTask = 4096;  // words per warp task
 #ifndef AG_BM_L2PF
 #define AG_BM_L2PF 0
 #endif
-constexpr int kBmRun = 8;           // consecutive words per lane per step
+#ifndef AG_BM_RUN
+#define AG_BM_RUN 8
+#endif
+constexpr int kBmRun = AG_BM_RUN;   // consecutive words per lane per step (a multiple of 4)
 constexpr int kBmSampleSteps = 2;   // steps of a task that sample exact keys (T is shared after)
 
 struct BmArgs {
@@ -455,9 +458,12 @@ __global__ void __launch_bounds__(kCostWarps * 32, AG_BM_MINB) k_bm_eval(const _
     const uint32_t ws = sub + kBmRun * lane;
     // streaming (evict-first) loads: the bitmap is read once and must not
     // push the prefix tables out of L2
-    if (A.vec && ws + kBmRun <= w1) {  // 16-byte aligned rows: two vector loads per run
-      const uint4 a = __ldcs((const uint4*)(row + ws)), b = __ldcs((const uint4*)(row + ws + 4));
-      v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
+    if (A.vec && ws + kBmRun <= w1) {  // 16-byte aligned rows: vector loads
+#pragma unroll
+      for (int h = 0; h < kBmRun / 4; ++h) {
+        const uint4 a = __ldcs((const uint4*)(row + ws + 4 * h));
+        v[4 * h] = a.x, v[4 * h + 1] = a.y, v[4 * h + 2] = a.z, v[4 * h + 3] = a.w;
+      }
     } else {
 #pragma unroll
       for (int u = 0; u < kBmRun; ++u) v[u] = ws + u < w1 ? __ldcs(row + ws + u) : 0u;
