@@ -18,8 +18,11 @@ import paper_2511_20975_b200 as P  # noqa: E402
 from paper_2511_20975_b200 import parallel as PL  # noqa: E402
 
 
+@pytest.mark.parametrize("bitmap", [False, True])
 @pytest.mark.parametrize("n,m,R,G", [(5, 8, 300, 4), (4, 5, 200, 3), (3, 4, 64, 8), (8, 12, 3, 4)])
-def test_shard_records_merge_equals_whole_space(n, m, R, G):
+def test_shard_records_merge_equals_whole_space(n, m, R, G, bitmap):
+    """bitmap: the shard records come straight from each shard's verdict
+    bitmap (ag_select_bitmap over [begin, end)) instead of its members."""
     space = P.ConfigSpace.chain(n, m)
     dev = P.Device(space)
     batch = P.AccuracyBatch.generate(space, P.GenParams(), R, seed=5 + n)
@@ -34,8 +37,8 @@ def test_shard_records_merge_equals_whole_space(n, m, R, G):
     recs, ranges = [], []
     for g in range(G):
         b, e = PL.shard_range(space.size, g, G)
-        res = dev.route_enumerate(truth, P.OracleRouter(), b, e)
-        recs.append(PL.shard_records(dev, res, R, load))
+        res = dev.route_enumerate(truth, P.OracleRouter(), b, e, bitmap=bitmap)
+        recs.append(PL.shard_records(dev, res, R, load, b, e))
         ranges.append(b)
         del res
     gathered = torch.stack(recs)
@@ -56,13 +59,15 @@ def test_sharded_path_world1_matches_whole_space():
     R = 200
     truth = P.AccuracyBatch.generate(space, P.GenParams(), R, seed=9).to_device()
     load = P.RuntimeCostContext([4] * 8, [i % 3 for i in range(8)], [8] * 8, [0.5 + 0.25 * i for i in range(8)])
-    res, total, before, (be, bc, bi) = PL.route_space_sharded(dev, truth, P.OracleRouter(), 0, 1, load)
-    ch, est = P.select_per_input(dev, res.indices, res.offsets, P.PER_INPUT_RUNTIME_COST, load)
-    torch.cuda.synchronize()
-    assert np.array_equal(total.cpu().numpy(), res.counts.cpu().numpy().astype(np.int64))
-    assert (before.cpu().numpy() == 0).all()
-    assert np.array_equal(bi.cpu().numpy().astype(np.uint32), ch.cpu().numpy().view(np.uint32))
-    assert np.array_equal(be.cpu().numpy(), est.cpu().numpy())
+    for out in (None, dev.alloc_route(R, 0, space.size, R * space.size, bitmap=True)):
+        res, total, before, (be, bc, bi) = PL.route_space_sharded(dev, truth, P.OracleRouter(), 0, 1, load,
+                                                                  out=out)
+        ch, est = P.select_per_input(dev, res.indices, res.offsets, P.PER_INPUT_RUNTIME_COST, load)
+        torch.cuda.synchronize()
+        assert np.array_equal(total.cpu().numpy(), res.counts.cpu().numpy().astype(np.int64))
+        assert (before.cpu().numpy() == 0).all()
+        assert np.array_equal(bi.cpu().numpy().astype(np.uint32), ch.cpu().numpy().view(np.uint32))
+        assert np.array_equal(be.cpu().numpy(), est.cpu().numpy())
 
 
 def test_async_select_errors_latch_until_synchronize():
