@@ -111,6 +111,7 @@ struct RoundShape {
 constexpr int kLookahead = 64;  // lookahead ring entries (a power of two)
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
+constexpr int kPruneInline = 768;  // int32 words of small dispatch data carried in the parameter block
 constexpr int kSmemNodes = 1024;
 constexpr int kPer = 4;  // FIFO positions per producer thread per chunk
 constexpr unsigned kFull = 0xffffffffu;
@@ -1619,6 +1620,10 @@ struct PruneArgs {
   uint64_t div_m;
   int32_t* status;
   uint32_t* ever;  // OR of every installed candidate-model mask (round validation)
+  // small dispatches: g_slot / g_begin / g_am travel in the parameter block
+  // (no staging copy, no wait for the previous one); g_* then point here
+  int inl;
+  int32_t inl_data[kPruneInline];
 };
 
 __device__ __forceinline__ uint32_t digit_p(uint32_t c, int a, const PruneArgs& A) {
@@ -1629,11 +1634,15 @@ __device__ __forceinline__ uint32_t digit_p(uint32_t c, int a, const PruneArgs& 
 // Request::mark_dispatched prefix pruning (request.cpp:70-86) for every
 // triple of one request, then its histogram / candidate masks from scratch.
 // With g_meta it first installs a new request's metadata (Request::make).
-__global__ void __launch_bounds__(256) k_sched_prune(PruneArgs A) {
+__global__ void __launch_bounds__(256) k_sched_prune(const __grid_constant__ PruneArgs A) {
   __shared__ uint32_t s_hist[kMaxAgents * 32];
   __shared__ int s_w[8], s_tot;
   const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const int s = A.g_slot[g];
+  const int G = gridDim.x;
+  const int32_t* g_slot = A.inl ? A.inl_data : A.g_slot;
+  const int32_t* g_begin = A.inl ? A.inl_data + G : A.g_begin;
+  const int32_t* g_am = A.inl ? A.inl_data + 2 * G + 1 : A.g_am;
+  const int s = g_slot[g];
   uint64_t vo;
   uint32_t len;
   if (A.g_meta) {
@@ -1649,8 +1658,8 @@ __global__ void __launch_bounds__(256) k_sched_prune(PruneArgs A) {
     len = A.nviable[s];
   }
   uint32_t* vl = A.pool + vo;
-  for (int t = A.g_begin[g]; t < A.g_begin[g + 1]; ++t) {
-    const int a = A.g_am[t] >> 8, mdl = A.g_am[t] & 0xFF;
+  for (int t = g_begin[g]; t < g_begin[g + 1]; ++t) {
+    const int a = g_am[t] >> 8, mdl = g_am[t] & 0xFF;
     // count survivors first: an empty result leaves the list untouched
     int c = 0;
     for (uint32_t q = tid; q < len; q += blockDim.x) c += (int)digit_p(vl[q], a, A) == mdl;
@@ -2114,6 +2123,8 @@ int flush_order(ag_sched* s) {
   return AG_OK;
 }
 
+int launch_prune_args(ag_sched* s, PruneArgs& A, int G, bool prep);
+
 int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vector<int32_t>& g_begin,
                  const std::vector<int32_t>& g_am, const std::vector<uint64_t>* meta) {
   ag_ctx* ctx = s->ctx;
@@ -2121,6 +2132,17 @@ int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vec
   if (G == 0) return AG_OK;
   int rc;
   const size_t n32 = (size_t)G + (G + 1) + g_am.size();
+  PruneArgs A;
+  if (!meta && n32 <= (size_t)kPruneInline) {
+    A.inl = 1;
+    std::memcpy(A.inl_data, g_slot.data(), 4 * (size_t)G);
+    std::memcpy(A.inl_data + G, g_begin.data(), 4 * (size_t)(G + 1));
+    if (!g_am.empty()) std::memcpy(A.inl_data + 2 * G + 1, g_am.data(), 4 * g_am.size());
+    A.g_slot = A.g_begin = A.g_am = nullptr;
+    A.g_meta = nullptr;
+    return launch_prune_args(s, A, G, false);
+  }
+  A.inl = 0;
   const size_t off_meta = (n32 * 4 + 15) & ~(size_t)15;
   const size_t bytes = off_meta + (meta ? meta->size() * 8 : 0);
   if ((rc = s->d_gam.ensure(bytes))) return rc;
@@ -2134,14 +2156,19 @@ int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vec
   if (!g_am.empty()) std::memcpy(h32 + 2 * G + 1, g_am.data(), 4 * g_am.size());
   if (meta) std::memcpy(h + off_meta, meta->data(), meta->size() * 8);
   AG_CUDA(cudaMemcpyAsync(s->d_gam.p, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
-  PruneArgs A;
-  A.N = s->N;
-  A.M = s->M;
   const int32_t* d = (const int32_t*)s->d_gam.p;
   A.g_slot = d;
   A.g_begin = d + G;
   A.g_am = d + 2 * G + 1;
   A.g_meta = meta ? (const uint64_t*)((const char*)s->d_gam.p + off_meta) : nullptr;
+  return launch_prune_args(s, A, G, meta != nullptr);
+}
+
+// the session's device arrays into A, then the launch (one block per group)
+int launch_prune_args(ag_sched* s, PruneArgs& A, int G, bool prep) {
+  ag_ctx* ctx = s->ctx;
+  A.N = s->N;
+  A.M = s->M;
   A.pool = (uint32_t*)s->d_pool.p;
   A.voff = (uint64_t*)s->d_voff.p;
   A.nviable = (uint32_t*)s->d_nv.p;
@@ -2154,7 +2181,7 @@ int launch_prune(ag_sched* s, const std::vector<int32_t>& g_slot, const std::vec
   A.status = (int32_t*)s->d_status.p;
   A.ever = (uint32_t*)((char*)s->d_status.p + 8);
   {
-    Launch L(ctx, meta ? K_SCHED_PREP : K_SCHED_APPLY);
+    Launch L(ctx, prep ? K_SCHED_PREP : K_SCHED_APPLY);
     k_sched_prune<<<G, 256, 0, ctx->stream>>>(A);
   }
   AG_CUDA(cudaGetLastError());

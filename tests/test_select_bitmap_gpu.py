@@ -42,7 +42,8 @@ def _both(dev, res, R, begin, end, kind, ctx):
     return ([t.cpu().numpy() for t in a], [t.cpu().numpy() for t in b])
 
 
-@pytest.mark.parametrize("n,m,R", [(5, 8, 600), (3, 4, 300), (6, 12, 24), (4, 3, 200), (2, 8, 100)])
+@pytest.mark.parametrize("n,m,R", [(5, 8, 600), (3, 4, 300), (6, 12, 24), (4, 3, 200), (2, 8, 100),
+                                   (16, 2, 40), (3, 40, 30), (9, 5, 6)])
 def test_matches_member_path(n, m, R):
     space = P.ConfigSpace.chain(n, m)
     dev = P.Device(space)
