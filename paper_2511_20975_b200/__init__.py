@@ -7,4 +7,4 @@ from .routing import (AccuracyBatch, ConfigSpace, Device, DeviceAccuracyBatch,  
 from .predictor import ConfigPredictor, PredictionBatch  # noqa: F401,E402
 from .scheduler import (PER_INPUT_RUNTIME_COST, PER_INPUT_STATIC, Assignment, Engines, Queue, audit_round_fairness,  # noqa: F401,E402
                         RuntimeCostContext, SchedSession, beam_schedule, select_bitmap, select_bitmap_stats,
-                        select_per_input, select_per_workflow)
+                        select_per_input, select_per_input_host, select_per_workflow)

@@ -347,10 +347,11 @@ int upload_truth(ag_ctx* ctx, const ag_truth* th, ag_truth* td) {
 
 extern "C" {
 
-// select_per_input_config for a batch of host AccurateSets: the members of
-// each set (oracle verdicts over the whole space, in canonical order) are
-// enumerated and compacted on the device, then re-costed and arg-minned there
-// (accuracy.cpp:227-238 + workload.cpp:149-176); only the choice comes back.
+// select_per_input_config for a batch of host AccurateSets: each set's
+// verdict bitmap over the whole space (oracle verdicts, canonical order) is
+// built on the device and the re-cost + arg-min runs straight from it
+// (accuracy.cpp:227-238 + workload.cpp:149-176; ag_select_bitmap: no member
+// list, no host round trip in between); only the choice comes back.
 int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* th, int32_t kind, const ag_load* load,
                              uint32_t* chosen, double* est) {
   agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
@@ -372,17 +373,10 @@ int ag_select_per_input_host(ag_ctx* ctx, const ag_truth* th, int32_t kind, cons
   ag_route_out o1{(uint32_t*)ctx->bitmap.p, (uint64_t*)ctx->counts.p, (uint64_t*)ctx->offsets.p,
                   nullptr, 0, nullptr};
   if ((rc = agb::route_enumerate(ctx, &td, &oracle, 0, S, 0, &o1))) return rc;
-  uint64_t tot = 0;
-  AG_CUDA(cudaMemcpyAsync(&tot, (uint64_t*)ctx->offsets.p + R, 8, cudaMemcpyDeviceToHost, ctx->stream));
-  AG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if ((rc = ctx->d_out_idx.ensure(4 * (size_t)tot + 4))) return rc;
-  if ((rc = agb::route_compact(ctx, R, 0, S, (const uint32_t*)ctx->bitmap.p,
-                               (const uint64_t*)ctx->offsets.p, (uint32_t*)ctx->d_out_idx.p, tot)))
-    return rc;
   uint32_t* d_chosen = (uint32_t*)ctx->d_sel.p;
   double* d_est = (double*)((char*)ctx->d_sel.p + ((4 * (size_t)R + 15) & ~(size_t)15));
-  if ((rc = ag_select_per_input(ctx, (const uint32_t*)ctx->d_out_idx.p, (const uint64_t*)ctx->offsets.p, R,
-                                kind, load, d_chosen, d_est)))
+  if ((rc = ag_select_bitmap(ctx, (const uint32_t*)ctx->bitmap.p, (const uint64_t*)ctx->counts.p, 0, S, R, kind,
+                             load, d_chosen, d_est, nullptr)))
     return rc;
   AG_CUDA(cudaMemcpyAsync(chosen, d_chosen, 4 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));
   if (est) AG_CUDA(cudaMemcpyAsync(est, d_est, 8 * (size_t)R, cudaMemcpyDeviceToHost, ctx->stream));

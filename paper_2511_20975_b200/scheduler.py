@@ -310,6 +310,22 @@ def select_bitmap(device: Device, bitmap, counts, begin: int, end: int, kind=PER
     return chosen[:R], est[:R]
 
 
+def select_per_input_host(device: Device, batch, kind=PER_INPUT_RUNTIME_COST, ctx=None):
+    """select_per_input_config for a host AccuracyBatch end to end
+    (ag_select_per_input_host: oracle verdict bitmaps over the whole space
+    built on the device, re-cost + arg-min straight from them).  Returns
+    numpy (chosen canonical index uint32 [R], estimate float64 [R])."""
+    R = batch.n_requests
+    chosen = np.zeros(max(R, 1), np.uint32)
+    est = np.zeros(max(R, 1), np.float64)
+    t = batch.c_struct()
+    load = ctx.c() if ctx is not None else None
+    check(lib().ag_select_per_input_host(device.handle, C.byref(t), kind,
+                                         C.byref(load) if load is not None else None,
+                                         C.c_void_p(_ptr(chosen)), C.c_void_p(_ptr(est))))
+    return chosen[:R], est[:R]
+
+
 def select_bitmap_stats(device: Device, enable: bool) -> int:
     """ag_select_bitmap_stats: start (enable) or stop counting the words the
     exact pass of select_bitmap evaluates; returns the count on stop."""

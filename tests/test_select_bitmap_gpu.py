@@ -149,3 +149,26 @@ def test_validation():
     empty = torch.zeros_like(res.bitmap)
     with pytest.raises(P.ValidationError):  # an empty accurate set
         P.select_bitmap(dev, empty, torch.zeros_like(counts), 0, space.size, P.PER_INPUT_STATIC, None)
+
+
+@pytest.mark.parametrize("n,m,R", [(5, 8, 300), (6, 12, 8), (3, 4, 100)])
+def test_host_entry_point_against_oracle(n, m, R):
+    """ag_select_per_input_host (the drop-in adapter's call for
+    select_per_input_config): host sets in, choices out, oracle-equal."""
+    space = P.ConfigSpace.chain(n, m)
+    dev = P.Device(space)
+    batch = P.AccuracyBatch.generate(space, P.GenParams(), R, seed=13)
+    res = _route(dev, batch, P.OracleRouter())
+    offs = res.offsets.cpu().numpy()
+    idx = res.indices.cpu().numpy().view(np.uint32)
+    for kind, ctx in ((P.PER_INPUT_RUNTIME_COST, _loads(m, 17)[2]), (P.PER_INPUT_STATIC, None)):
+        ch, est = P.select_per_input_host(dev, batch, kind, ctx)
+        for r in range(0, R, max(1, R // 25)):
+            if kind == P.PER_INPUT_STATIC:
+                want, west = O.select_per_input(n, m, space.cost, [0] * m, [0] * m, [1] * m, [1.0] * m, 0,
+                                                idx[offs[r]:offs[r + 1]])
+                assert ch[r] == want
+            else:
+                want, west = O.select_per_input(n, m, space.cost, ctx.occupancy, ctx.queued_ahead, ctx.slots,
+                                                ctx.mean, 1, idx[offs[r]:offs[r + 1]])
+                assert ch[r] == want and est[r] == west
