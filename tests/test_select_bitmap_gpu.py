@@ -5,7 +5,10 @@ bit-exact chosen index and fp64 estimate, static and runtime-cost kinds,
 shard ranges that start and end mid-word and mid-prefix, the noisy router,
 random loads that reorder the tiers, and the reference's ValidationErrors
 (workload.cpp:140-156)."""
+import json
 import math
+import os
+import subprocess
 
 import numpy as np
 import pytest
@@ -172,3 +175,41 @@ def test_host_entry_point_against_oracle(n, m, R):
                 want, west = O.select_per_input(n, m, space.cost, ctx.occupancy, ctx.queued_ahead, ctx.slots,
                                                 ctx.mean, 1, idx[offs[r]:offs[r + 1]])
                 assert ch[r] == want and est[r] == west
+
+
+REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "ref_bench")
+
+
+@pytest.mark.parametrize("n,m,R", [(5, 8, 2000), (7, 12, 4), (8, 12, 4)])
+def test_digest_matches_unmodified_reference(n, m, R):
+    """The unmodified reference's select_per_input_config over the exhaustive
+    accurate sets (oracle/_ref/ref_bench select: at_index + accurate, the
+    (static_cost, models) sort, strict-< scan of estimate_completion) against
+    the bitmap path on the same generator output: digest of (chosen index,
+    estimate bits) per request.  (8, 12) is the config-4 space at full size
+    (4.3e8 configurations per request; 4 of its 16 requests, so that the
+    reference's Configuration vectors fit in host memory) and (7, 12) the
+    same shape one agent shorter: the prefix bounds prune all but a few
+    words there."""
+    if not os.path.exists(REF):
+        pytest.skip("oracle/_ref/ref_bench not built")
+    from paper_2511_20975_b200 import workloads as W
+
+    seed = 1
+    out = subprocess.run([REF, "select", str(n), str(m), str(R), str(os.cpu_count() or 1), str(seed), "exhaustive"],
+                         capture_output=True, text=True, check=True, timeout=900).stdout
+    ref = json.loads(out.strip().splitlines()[-1])
+    space = P.ConfigSpace.chain(n, m)
+    dev = P.Device(space)
+    batch = P.AccuracyBatch.generate(space, P.GenParams(), R, seed)
+    res = _route(dev, batch, P.OracleRouter())
+    mean = [0.05 + math.exp((-0.3 + 0.35 * i) + 0.5 * 0.25 * 0.25) for i in range(m)]
+    ctx = P.RuntimeCostContext([4] * m, [i % 3 for i in range(m)], [8] * m, mean)
+    ch, est = P.select_bitmap(dev, res.bitmap, res.counts[:R], 0, space.size, P.PER_INPUT_RUNTIME_COST, ctx)
+    ch = ch.cpu().numpy().view(np.uint32)
+    bits = est.cpu().numpy().view(np.uint64)
+    d = 0x5EED
+    for r in range(R):
+        d = W.mix(d, int(ch[r]), int(bits[r]))
+    assert int(res.counts.sum().item()) == ref["configs_costed"]
+    assert f"{d:016x}" == ref["digest"]
