@@ -509,14 +509,14 @@ def run_config5(horizon=240.0):
     scen = os.path.join(INTEG, "proj", "scenarios", "reference.json")
     if not (os.path.exists(ref_bin) and os.path.exists(gpu_bin) and os.path.exists(scen)):
         return None
-    pts, same = [], True
-    with tempfile.TemporaryDirectory() as td:
-        for rate in C5_RATES:
+    def sweep(scenario, rates, hz, td):
+        rows, ok = [], True
+        for rate in rates:
             row = {"rate": rate}
             outs = []
             for kind, b in (("reference", ref_bin), ("gpu", gpu_bin)):
                 out = os.path.join(td, f"{kind}_{rate}.jsonl")
-                r = subprocess.run([b, scen, "aragog", out, "--horizon", str(horizon), "--rate",
+                r = subprocess.run([b, scenario, "aragog", out, "--horizon", str(hz), "--rate",
                                     str(rate)], capture_output=True, text=True, check=True)
                 j = json.loads(r.stdout.strip().splitlines()[-1])
                 row[kind] = {"rounds": j["rounds"], "requests": j["requests"],
@@ -524,8 +524,22 @@ def run_config5(horizon=240.0):
                              "gpu_launches": j["gpu_launches"]}
                 outs.append(open(out, "rb").read())
             row["trace_identical"] = outs[0] == outs[1]
-            same &= row["trace_identical"]
-            pts.append(row)
+            ok &= row["trace_identical"]
+            rows.append(row)
+        return rows, ok
+
+    with tempfile.TemporaryDirectory() as td:
+        pts, same = sweep(scen, C5_RATES, horizon, td)
+    # decompose.json (the diamond workflow: plan -> {search, math} -> synth)
+    # over its own shipped sweep rates and horizon
+    decompose = None
+    dscen = os.path.join(INTEG, "proj", "scenarios", "decompose.json")
+    if os.path.exists(dscen):
+        dsw = json.load(open(dscen)).get("sweep", {})
+        with tempfile.TemporaryDirectory() as td:
+            dpts, dsame = sweep(dscen, dsw.get("rates", [1.0]), dsw.get("horizon", 180), td)
+        decompose = {"points": dpts, "traces_identical": dsame}
+        same &= dsame
     # BASELINE scale: a 5-stage chain x 8 tiers scenario (the config-2 space)
     # with ~500-960 requests queued per round, drained
     scale = None
@@ -562,10 +576,10 @@ def run_config5(horizon=240.0):
         same &= row["trace_identical"]
         scale = row
     return {"workload": f"config5: reference.json under run_simulation, horizon {horizon:g} s, "
-                        f"aragog policy, rates {list(C5_RATES)} req/s; reference build vs the "
-                        "same sources relinked with the GPU adapter; plus a 5x8 scenario at "
-                        "BASELINE scale",
-            "traces_identical": same, "points": pts, "scale": scale,
+                        f"aragog policy, rates {list(C5_RATES)} req/s, and decompose.json over its "
+                        "own sweep; reference build vs the same sources relinked with the GPU "
+                        "adapter; plus a 5x8 scenario at BASELINE scale",
+            "traces_identical": same, "points": pts, "scale": scale, "decompose": decompose,
             "note": "single-request decisions through the C ABI: each predict / round is one "
                     "launch + synchronisation, so tiny queues are launch-latency bound"}
 
@@ -967,6 +981,10 @@ def summarize(line, sched, deep, noisy, linear, chain, config5, select=None, con
                           "rounds_per_s": [[p["rate"], _r(p["gpu"]["rounds_per_s"]),
                                             _r(p["reference"]["rounds_per_s"])]
                                            for p in config5["points"]]}
+        if config5.get("decompose"):
+            out["config5"]["decompose"] = [[p["rate"], _r(p["gpu"]["rounds_per_s"]),
+                                            _r(p["reference"]["rounds_per_s"]), p["trace_identical"]]
+                                           for p in config5["decompose"]["points"]]
         if config5.get("scale"):
             sc = config5["scale"]
             out["config5"]["scale_5x8"] = [sc["trace_identical"], _r(sc["gpu"]["wall_s"]),
