@@ -111,7 +111,8 @@ struct RoundShape {
 constexpr int kLookahead = 64;  // lookahead ring entries (a power of two)
 constexpr int kMaxBeam = 32;
 constexpr int kMaxEng = 32;
-constexpr int kPruneInline = 768;  // int32 words of small dispatch data carried in the parameter block
+constexpr int kPruneInline = 768;
+constexpr int kInlineRec = 48;  // refresh records carried in the round's parameter block  // int32 words of small dispatch data carried in the parameter block
 constexpr int kSmemNodes = 1024;
 constexpr int kPer = 4;  // FIFO positions per producer thread per chunk
 constexpr unsigned kFull = 0xffffffffu;
@@ -168,6 +169,8 @@ struct RoundArgs {
   // round input deltas in mapped pinned host memory (or a DMA'd copy)
   const int4* h_rec;      // refresh records {pos (-1: none), slot, ready lo, ready hi}
   int n_rec;
+  int n_inl;              // 1: the records are inl_rec (a small batch in the parameter block:
+  int4 inl_rec[kInlineRec];  // no PCIe read on the round's critical path)
   const int32_t* h_cidx;  // [Q] or null
   uint4* pinfo;           // [Q] per-position pair records (see the setup)
   int8_t prio[64];
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(256) k_sched_refresh(const int4* __restrict__ 
 }
 
 template <int BM>
-__global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(RoundArgs A) {
+__global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(const __grid_constant__ RoundArgs A) {
   constexpr int kRoundThreads = RoundShape<BM>::threads, kProducers = RoundShape<BM>::producers;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ int s_occ[2][kMaxBeam][kMaxEng];
@@ -568,7 +571,8 @@ __global__ void __launch_bounds__(RoundShape<BM>::threads, 1) k_sched_round(Roun
           if (i < A.Q) A.cidx[i] = v[u];
         }
       }
-    apply_records(A.h_rec, A.n_rec, tid, kRoundThreads, N, A.ready, A.cand, A.nviable, A.order, A.pinfo,
+    apply_records(A.n_inl ? A.inl_rec : A.h_rec, A.n_rec, tid, kRoundThreads, N, A.ready, A.cand, A.nviable,
+                  A.order, A.pinfo,
                   [&](int ag) { return (int)A.prio_rank[ag]; });
   }
   __syncthreads();
@@ -2463,6 +2467,10 @@ int run_round(ag_sched* s, const ag_engines* engines, int B, const int32_t* cidx
   A.ever = (const uint32_t*)((char*)s->d_status.p + 8);
   A.h_rec = (const int4*)hd;
   A.n_rec = (int)n_rec;
+  if (!cidx_host && n_rec <= (size_t)kInlineRec) {
+    std::memcpy(A.inl_rec, h, n_rec * 16);
+    A.n_inl = 1;
+  }
   A.h_cidx = cidx_host ? (const int32_t*)(hd + off_cidx) : nullptr;
   A.pinfo = (uint4*)s->d_pinfo.p;
   std::memcpy(A.prio, s->prio, sizeof A.prio);
