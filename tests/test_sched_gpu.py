@@ -431,3 +431,32 @@ def test_session_pool_is_a_capacity():
         for s, r in mirror.items():
             assert sess.viable(s).tolist() == r["viable"], (it, s)
     assert added > 4 * 600
+
+
+@pytest.mark.parametrize("k", [40, 300])
+def test_dispatch_small_and_large_batches_match_oracle(k):
+    """ag_sched_dispatch carries small batches in the prune kernel's parameter
+    block and stages large ones (more than 768 words of slot / range /
+    agent-model data) through pinned memory: both prune every dispatched
+    request's viable list exactly as Request::mark_dispatched's prefix prune
+    (request.cpp:70-86)."""
+    rng = np.random.default_rng(k)
+    n, m = 3, 4
+    sp = P.ConfigSpace.chain(n, m)
+    dev = P.Device(sp)
+    sess = P.SchedSession(dev, k, k * 40)
+    reqs = []
+    for i in range(k):
+        v = sorted(set(int(x) for x in rng.integers(0, sp.size, int(rng.integers(5, 30)))))
+        reqs.append(dict(id=i, arrival=float(i), stages=[READY, 0, 0], viable=v))
+    slots = sess.add(P.Queue(n, [r["id"] for r in reqs], [r["arrival"] for r in reqs],
+                             [s for r in reqs for s in r["stages"]], [r["viable"] for r in reqs]))
+    trip, tslots = [], []
+    for s, r in zip(slots, reqs):
+        mdl = int((r["viable"][int(rng.integers(0, len(r["viable"])))] // m ** (n - 1)) % m)
+        trip.append((0, r["id"], 0, mdl))
+        tslots.append(int(s))
+        r["viable"] = [int(x) for x in O.prefix_prune(n, m, r["viable"], 0, mdl)]
+    sess.dispatch(P.Assignment(trip, [], 0.0, 0.0, 0, 0, tslots))
+    for s, r in zip(slots, reqs):
+        assert sess.viable(int(s)).tolist() == r["viable"]
