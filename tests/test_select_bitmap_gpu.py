@@ -213,3 +213,47 @@ def test_digest_matches_unmodified_reference(n, m, R):
         d = W.mix(d, int(ch[r]), int(bits[r]))
     assert int(res.counts.sum().item()) == ref["configs_costed"]
     assert f"{d:016x}" == ref["digest"]
+
+
+def test_randomised_spaces_ranges_and_loads():
+    """Randomised cross-check of the bitmap path against the member path:
+    chain spaces of 2-8 agents and 2-16 tiers, oracle or noisy verdicts,
+    random shard ranges (records) and whole-space selections, random loads
+    (including negative and tied estimate terms), both policy kinds."""
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        n = int(rng.integers(2, 9))
+        m = int(rng.integers(2, 17))
+        while m ** n > 2_000_000:
+            n -= 1
+        space = P.ConfigSpace.chain(n, m)
+        dev = P.Device(space)
+        R = int(rng.integers(1, 40))
+        batch = P.AccuracyBatch.generate(space, P.GenParams(), R, seed=int(rng.integers(1, 1 << 30)))
+        router = P.OracleRouter() if case % 2 == 0 else P.NoisyRouter(float(rng.uniform(0, 0.2)),
+                                                                        float(rng.uniform(0, 0.4)),
+                                                                        int(rng.integers(1, 1000)))
+        if case % 3 == 2:
+            b = int(rng.integers(0, space.size // 2))
+            e = int(rng.integers(b + 1, space.size + 1))
+        else:
+            b, e = 0, space.size
+        res = _route(dev, batch, router, b, e)
+        slots = rng.integers(1, 9, m).tolist()
+        occ = [int(rng.integers(0, s + 1)) for s in slots]
+        queued = rng.integers(0, 20, m).tolist()
+        mean = (rng.choice([0.5, 1.0, 2.0], m) if case % 4 == 1 else rng.uniform(-1.0, 10.0, m)).tolist()
+        ctx = P.RuntimeCostContext(occ, queued, slots, mean)
+        for kind, c in ((P.PER_INPUT_RUNTIME_COST, ctx), (P.PER_INPUT_STATIC, None)):
+            rec_bm = torch.zeros((R, 4), dtype=torch.int64, device=dev.torch_device)
+            P.select_bitmap(dev, res.bitmap, res.counts[:R], b, e, kind, c, check_errors=False, records=rec_bm)
+            if kind == P.PER_INPUT_RUNTIME_COST:
+                from paper_2511_20975_b200 import parallel as PL
+
+                rec_mem = PL.shard_records(dev, P.RouteResult(res.counts, res.offsets, res.indices, None), R, c)
+                torch.cuda.synchronize()
+                assert torch.equal(rec_bm, rec_mem), case
+            if bool((res.counts[:R] > 0).all()):
+                (ca, ea), (cb, eb) = _both(dev, res, R, b, e, kind, c)
+                assert np.array_equal(ca, cb), case
+                assert np.array_equal(ea.view(np.int64), eb.view(np.int64)), case
