@@ -329,7 +329,12 @@ __global__ void __launch_bounds__(256) k_merge_records(const uint64_t* __restric
 // member list (4 B per member).
 // The prefix level k is chosen so that a 32-bit word spans at most two
 // prefixes (M^(N-k) >= 32).
-constexpr uint32_t kBmTask = 4096;  // words per warp task
+// words per warp task: a power of two between kBmTaskMin and kBmTaskMax
+// chosen per call so that the batch is about kBmTasksTarget tasks -- long
+// tasks amortise the per-task start (a deep space: 2,048 words at config 4),
+// short ones spread a batch of small rows over more warps (256 at config 3)
+constexpr uint32_t kBmTaskMin = 256, kBmTaskMax = 4096;
+constexpr uint64_t kBmTasksTarget = 1 << 16;
 #ifndef AG_BM_MINB
 #define AG_BM_MINB 3
 #endif
@@ -348,6 +353,7 @@ struct BmArgs {
   const uint64_t* counts;  // [R]
   uint64_t begin, end;
   uint32_t W, n_pre;
+  uint32_t task_words;      // words per warp task (a multiple of 32 * kBmRun)
   int vec;                 // rows 16-byte aligned (vector loads)
   int R, tpr;              // tasks per request
   int kind, any_missing, allow_empty;
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(kCostWarps * 32, AG_BM_MINB) k_bm_eval(const _
   const int t = blockIdx.x * kCostWarps + wid;
   if (t >= A.R * A.tpr) return;
   const int r = t / A.tpr;
-  const uint32_t w0 = (uint32_t)(t - r * A.tpr) * kBmTask, w1 = min(A.W, w0 + kBmTask);
+  const uint32_t w0 = (uint32_t)(t - r * A.tpr) * A.task_words, w1 = min(A.W, w0 + A.task_words);
   const uint32_t* row = A.bitmap + (size_t)r * A.W;
   const bool runtime = A.kind != 0, check_nan = A.any_missing != 0;
   const uint32_t mk = A.mk;
@@ -822,7 +828,12 @@ int select_bitmap_impl(ag_ctx* ctx, const uint32_t* bitmap, const uint64_t* coun
   A.end = end;
   const uint64_t W = (end - begin + 31) / 32;
   A.W = (uint32_t)W;
-  A.tpr = (int)std::max<uint64_t>(1, (W + kBmTask - 1) / kBmTask);
+  {
+    uint32_t tw = kBmTaskMin;
+    while (tw < kBmTaskMax && (uint64_t)R * W / (2 * tw) >= kBmTasksTarget) tw *= 2;
+    A.task_words = tw;
+  }
+  A.tpr = (int)std::max<uint64_t>(1, (W + A.task_words - 1) / A.task_words);
   if ((uint64_t)R * (uint64_t)A.tpr >= (1ull << 31)) return fail(AG_ERR_VALIDATION, "batch too large for one launch");
   A.R = R;
   A.kind = kind == AG_POLICY_PER_INPUT_RUNTIME_COST ? 1 : 0;
