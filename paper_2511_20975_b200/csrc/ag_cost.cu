@@ -32,7 +32,12 @@ namespace agb {
 namespace {
 
 constexpr int kCostWarps = 8;
-constexpr uint64_t kTask = 1 << 13;     // members per task (at least; a power of two)
+// members per task: a power of two from kTask up to kTaskMax, the largest
+// that still leaves about kTaskTarget tasks (2^15 members at config 4,
+// 2^11 at config 3; the fixed-size sweep is in DESIGN.md §5)
+constexpr uint64_t kTask = 1 << 11;
+constexpr uint64_t kTaskMax = 1 << 16;
+constexpr uint64_t kTaskTarget = 1 << 15;
 constexpr int kPlanSmemReq = 24 * 1024;  // requests whose offsets the plan stages in shared memory
 constexpr uint64_t kTaskCap = 1 << 20;  // tasks per call beyond one per request
 constexpr uint64_t kPrefixMax = 1u << 22;  // prefix-table entries (64 MB)
@@ -94,8 +99,8 @@ __global__ void __launch_bounds__(256) k_cost_prefix(const __grid_constant__ Cos
 }
 
 // The task plan on the device (no host round trip): request r owns tasks
-// [r_task[r], r_task[r+1]), one per tsize members (kTask, or more when the
-// batch holds over kTaskCap * kTask members, so at most R + kTaskCap tasks);
+// [r_task[r], r_task[r+1]), one per tsize members (see kTask; more when the
+// batch holds over kTaskCap * tsize members, so at most R + kTaskCap tasks);
 // an empty set latches "accurate set is empty" (workload.cpp:151-156) and
 // gets no task.
 __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ CostArgs A) {
@@ -111,6 +116,7 @@ __global__ void __launch_bounds__(1024) k_cost_plan(const __grid_constant__ Cost
   const uint64_t total = off(A.R) - off(0);
   const uint64_t tq = (total + kTaskCap - 1) / kTaskCap;
   uint64_t ts = kTask;
+  while (ts < kTaskMax && total / (2 * ts) >= kTaskTarget) ts <<= 1;
   while (ts < tq) ts <<= 1;
   const int sh = __ffsll((long long)ts) - 1;
   if (tid == 0) *A.tsize = ts;
