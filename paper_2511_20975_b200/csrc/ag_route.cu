@@ -873,7 +873,7 @@ cudaError_t launch_request_scan(ag_ctx* ctx, cudaStream_t s, const uint64_t* cou
 }
 
 // K3: stream compaction of the verdict bitmap into canonical-order indices.
-// Work unit = kUnitGroups groups of 32 words (each group's output offset is
+// Work unit = unit_groups_for(W) groups of 32 words (each group's output offset is
 // known from K2a); persistent warps stride over units.  Per iteration the warp
 // loads 32 words (coalesced, software-pipelined) and scans their popcounts;
 // the members are staged bit-parallel in shared memory -- for word w lane j
@@ -883,16 +883,22 @@ cudaError_t launch_request_scan(ag_ctx* ctx, cudaStream_t s, const uint64_t* cou
 // full 16-byte vector is written back at once; the <= 3 trailing members carry
 // over to the next iteration, so global stores are almost all full vectors.
 constexpr int kStage = 32 * 32 + 8;  // one iteration's members + carry + pad
+// groups per unit: 4 for rows of up to 2^16 words (config 2: finer units
+// balance the per-request density spread), 16 for deep rows (config 4: the
+// per-unit start amortised over more words); AG_UNIT_GROUPS forces one
+// (scripts/compact_sweep*.sh, profiles/r02w_compact_unit_sweep.txt)
 #ifndef AG_UNIT_GROUPS
-#define AG_UNIT_GROUPS 4
+#define AG_UNIT_GROUPS 0
 #endif
-constexpr uint32_t kUnitGroups = AG_UNIT_GROUPS;
+__host__ __device__ constexpr uint32_t unit_groups_for(uint32_t W) {
+  return AG_UNIT_GROUPS > 0 ? (uint32_t)AG_UNIT_GROUPS : (W <= (1u << 16) ? 4u : 16u);
+}
 
 __global__ void __launch_bounds__(kThreads)
     k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ group_off,
                     const uint64_t* __restrict__ offsets, uint64_t begin, uint32_t W, uint32_t C,
                     uint32_t units_per_req, uint64_t div_u, int R, uint32_t* __restrict__ indices,
-                    uint64_t capacity) {
+                    uint64_t capacity, uint32_t ug) {
   __shared__ __align__(16) uint32_t s_stage[kWarpsPerBlock][kStage];
   __shared__ __align__(16) uint32_t s_word[kWarpsPerBlock][32];
   __shared__ __align__(16) uint32_t s_pre[kWarpsPerBlock][32];
@@ -906,7 +912,7 @@ __global__ void __launch_bounds__(kThreads)
   // while the current one is processed (two dependent global loads)
   auto unit_of = [&](uint64_t unit, uint32_t& r, uint32_t& g0) {
     r = units_per_req == 1 ? (uint32_t)unit : (uint32_t)__umul64hi(unit, div_u);
-    g0 = ((uint32_t)unit - r * units_per_req) * kUnitGroups;  // first group (32 words each)
+    g0 = ((uint32_t)unit - r * units_per_req) * ug;  // first group (32 words each)
   };
   uint64_t unit = (uint64_t)blockIdx.x * kWarpsPerBlock + wid;
   uint64_t gs_next = 0;
@@ -919,7 +925,7 @@ __global__ void __launch_bounds__(kThreads)
     uint32_t r, g0;
     unit_of(unit, r, g0);
     const uint32_t wbeg = g0 * 32;
-    const uint32_t wend = min(W, wbeg + 32 * kUnitGroups);
+    const uint32_t wend = min(W, wbeg + 32 * ug);
     // global output position of the unit's first member
     const uint64_t gs = gs_next;
     if (unit + nwarps < units) {
@@ -1108,7 +1114,7 @@ int make_router(const ag_router* r, RouterDev* out) {
   return AG_OK;
 }
 
-// K3 launch: persistent warps over units of kUnitGroups groups, the grid
+// K3 launch: persistent warps over units of unit_groups_for(W) groups, the grid
 // sized to the device's resident capacity for this kernel.
 int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, const uint32_t* bitmap,
                    const uint64_t* offsets, uint32_t* indices, uint64_t capacity) {
@@ -1120,14 +1126,15 @@ int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, c
     resident = std::max(1, sms * per_sm);
   }
   const uint32_t ngroups = (W + 31) / 32;
-  const uint32_t upr = (ngroups + kUnitGroups - 1) / kUnitGroups;
+  const uint32_t ug = unit_groups_for(W);
+  const uint32_t upr = (ngroups + ug - 1) / ug;
   const uint64_t units = (uint64_t)R * upr;
   if (units >= (1ULL << 32)) return fail(AG_ERR_VALIDATION, "batch too large for one launch");
   const uint64_t want = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)resident));
   Launch L(ctx, K_ROUTE_COMPACT);
   AG_CUDA(launch_pdl(k_route_compact, blocks, kThreads, 0, ctx->stream, bitmap, (const uint64_t*)ctx->chunk_off.p,
-                     offsets, begin, W, C, upr, magic_div(upr), R, indices, capacity));
+                     offsets, begin, W, C, upr, magic_div(upr), R, indices, capacity, ug));
   return AG_OK;
 }
 
