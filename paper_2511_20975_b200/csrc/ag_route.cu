@@ -890,15 +890,16 @@ constexpr int kStage = 32 * 32 + 8;  // one iteration's members + carry + pad
 #ifndef AG_UNIT_GROUPS
 #define AG_UNIT_GROUPS 0
 #endif
-__host__ __device__ constexpr uint32_t unit_groups_for(uint32_t W) {
+constexpr uint32_t unit_groups_for(uint32_t W) {  // 2, 4, 8 or 16 (instantiated)
   return AG_UNIT_GROUPS > 0 ? (uint32_t)AG_UNIT_GROUPS : (W <= (1u << 16) ? 4u : 16u);
 }
 
+template <uint32_t ug>
 __global__ void __launch_bounds__(kThreads)
     k_route_compact(const uint32_t* __restrict__ bitmap, const uint64_t* __restrict__ group_off,
                     const uint64_t* __restrict__ offsets, uint64_t begin, uint32_t W, uint32_t C,
                     uint32_t units_per_req, uint64_t div_u, int R, uint32_t* __restrict__ indices,
-                    uint64_t capacity, uint32_t ug) {
+                    uint64_t capacity) {
   __shared__ __align__(16) uint32_t s_stage[kWarpsPerBlock][kStage];
   __shared__ __align__(16) uint32_t s_word[kWarpsPerBlock][32];
   __shared__ __align__(16) uint32_t s_pre[kWarpsPerBlock][32];
@@ -1122,7 +1123,7 @@ int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, c
   if (!resident) {
     int sms = 0, per_sm = 0;
     AG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
-    AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_route_compact, kThreads, 0));
+    AG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_route_compact<4>, kThreads, 0));
     resident = std::max(1, sms * per_sm);
   }
   const uint32_t ngroups = (W + 31) / 32;
@@ -1133,8 +1134,10 @@ int launch_compact(ag_ctx* ctx, int R, uint32_t W, uint32_t C, uint64_t begin, c
   const uint64_t want = (units + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)resident));
   Launch L(ctx, K_ROUTE_COMPACT);
-  AG_CUDA(launch_pdl(k_route_compact, blocks, kThreads, 0, ctx->stream, bitmap, (const uint64_t*)ctx->chunk_off.p,
-                     offsets, begin, W, C, upr, magic_div(upr), R, indices, capacity, ug));
+  auto* kern = ug == 16 ? k_route_compact<16> : ug == 8 ? k_route_compact<8> : ug == 2 ? k_route_compact<2>
+                                                                               : k_route_compact<4>;
+  AG_CUDA(launch_pdl(kern, blocks, kThreads, 0, ctx->stream, bitmap, (const uint64_t*)ctx->chunk_off.p, offsets,
+                     begin, W, C, upr, magic_div(upr), R, indices, capacity));
   return AG_OK;
 }
 
