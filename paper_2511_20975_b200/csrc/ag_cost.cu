@@ -335,7 +335,8 @@ __global__ void __launch_bounds__(256) k_merge_records(const uint64_t* __restric
 // member list (4 B per member).
 // The prefix level k is chosen so that a 32-bit word spans at most two
 // prefixes (M^(N-k) >= 32).
-// words per warp task: a power of two between kBmTaskMin and kBmTaskMax
+//
+// Words per warp task: a power of two between kBmTaskMin and kBmTaskMax
 // chosen per call so that the batch is about kBmTasksTarget tasks -- long
 // tasks amortise the per-task start (a deep space: 2,048 words at config 4),
 // short ones spread a batch of small rows over more warps (256 at config 3)
@@ -946,7 +947,7 @@ extern "C" int ag_select_bitmap(ag_ctx* ctx, const uint32_t* bitmap, const uint6
 }
 
 extern "C" int ag_select_bitmap_stats(ag_ctx* ctx, int32_t enable, uint64_t* words_evaluated) {
-  // diagnostics: count the words pass 2 of ag_select_bitmap evaluates
+  // diagnostics: count the queued words ag_select_bitmap re-costs exactly
   agb::DeviceGuard device_guard(ctx ? ctx->device : -1);
   if (!ctx) return fail(AG_ERR_VALIDATION, "null argument");
   if (enable) {
